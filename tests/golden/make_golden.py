@@ -1,0 +1,353 @@
+"""Generate the golden parity fixtures by running the REFERENCE itself.
+
+Run in the build container (where /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+It imports the reference package `vlz` read-only from /root/reference/pkg/src
+and records its outputs for seeded inputs into tests/golden/*.npz (+ .json).
+Nothing at test time reads /root/reference; the fixtures are self-contained
+(inputs are stored, or regenerated from seeded generators for the full-size
+hash pins).
+
+Fixture groups
+  corpus.npz      dualquant_vector streams for ~90 seeded arrays x configs
+                  (1D/2D/3D, b 8..64, all 10 padding policies, radius 2..32768,
+                  eb 1e-2..1e-5, partial blocks, tiny shapes, tie-rich and
+                  narrowing-heavy data) + compress() container bytes + the
+                  reference decompress() output for the small ones.
+  errors.json     error precedence/index cases (non-finite, overflow, eb<=0).
+  corrupt.npz     decompression stream-corruption cases + expected exception.
+  known.json      hand known-answer cases lifted from the reference tests.
+  fullsize.json   sha256 of the reference streams for C1/C2 at full size
+                  (regenerated data via paper_2201_04614_b200.workloads).
+"""
+
+from __future__ import annotations
+
+import hashlib
+import io
+import json
+import math
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, REPO)
+
+import vlz  # noqa: E402  (the reference, read-only)
+import vlz.model as vmodel  # noqa: E402
+from vlz import errors as verr  # noqa: E402
+from vlz.container import deserialize  # noqa: E402
+from vlz.kernel import dualquant_scalar  # noqa: E402
+from vlz.model import CompressionConfig, ErrorBound, PaddingPolicy  # noqa: E402
+from vlz.pipeline import compress, decompress  # noqa: E402
+from vlz.reconstruct import decompress_parsed, reconstruct_block  # noqa: E402
+from vlz.vector import dualquant_vector  # noqa: E402
+
+from paper_2201_04614_b200 import workloads  # noqa: E402
+
+POLICIES = [
+    "zero",
+    "min:global", "max:global", "mean:global",
+    "min:block", "max:block", "mean:block",
+    "min:edge", "max:edge", "mean:edge",
+]
+
+# allow block edge 256 (BASELINE config 1); the reference reads this module
+# global at call time (model.py:149,212)
+vmodel.VALID_BLOCK_EDGES = (8, 16, 32, 64, 256)
+
+
+def _smooth(rng, shape):
+    offset = rng.uniform(-700, 700)
+    amp = rng.uniform(1.0, 40.0)
+    axes = [np.linspace(0.0, rng.uniform(1, 8), s) for s in shape]
+    mesh = np.add.reduce(np.meshgrid(*axes, indexing="ij"))
+    field = offset + amp * np.sin(mesh) + 0.05 * amp * np.cos(3.0 * mesh)
+    return np.clip(field, -1e3, 1e3).astype(np.float32)
+
+
+def _noise(rng, shape):
+    return rng.uniform(-1e3, 1e3, shape).astype(np.float32)
+
+
+def _ties(rng, shape, eb):
+    # values exactly on quantization half-points (k + 0.5) * 2eb where
+    # representable, plus exact grid points: stresses round-half-away
+    k = rng.integers(-2000, 2000, size=shape).astype(np.float64)
+    half = rng.random(shape) < 0.5
+    return ((k + np.where(half, 0.5, 0.0)) * (2.0 * eb)).astype(np.float32)
+
+
+def _narrow(rng, shape):
+    # |v| ~ 1e3..4e3 with eb 1e-5: ulp32(v) > eb, so the float32-narrowing
+    # bound check fires often and |q| is ~1e8 (exact fp64 path)
+    return rng.uniform(1000.0, 4000.0, shape).astype(np.float32) * np.where(
+        rng.random(shape) < 0.5, -1, 1
+    ).astype(np.float32)
+
+
+def _big_q(rng, shape, eb):
+    # |q| just below the 2^31-1 overflow guard
+    lim = (2**31 - 2) * 2.0 * eb
+    return (rng.uniform(-1.0, 1.0, shape) * lim).astype(np.float32)
+
+
+def _cfg(eb, b, pol, radius, lanes=8):
+    return CompressionConfig(
+        ErrorBound.absolute(eb), block_edge=b, lane_width=lanes,
+        padding=PaddingPolicy.parse(pol), radius=radius,
+    )
+
+
+class Store:
+    def __init__(self):
+        self.arrays = {}
+        self.meta = []
+
+    def add(self, meta: dict, **arrays):
+        i = len(self.meta)
+        meta = dict(meta)
+        meta["id"] = i
+        self.meta.append(meta)
+        for k, v in arrays.items():
+            self.arrays[f"{i}.{k}"] = v
+
+    def save(self, name):
+        self.arrays["meta"] = np.frombuffer(json.dumps(self.meta).encode(), dtype=np.uint8)
+        np.savez_compressed(os.path.join(HERE, name), **self.arrays)
+        print(f"wrote {name}: {len(self.meta)} cases")
+
+
+def stream_case(store, data, eb, b, pol, radius, tag, with_blob):
+    cfg = _cfg(eb, b, pol, radius)
+    try:
+        s = dualquant_vector(data, cfg)
+    except verr.VlzError as exc:  # pragma: no cover - corpus avoids errors
+        raise RuntimeError(f"unexpected reference error {exc!r} for {tag}")
+    arrays = dict(
+        data=data,
+        codes=s.codes.astype(np.uint16),
+        outlier_values=s.outlier_values,
+        outlier_counts=s.outlier_counts,
+        scalars=s.scalars.values,
+    )
+    meta = dict(tag=tag, shape=list(data.shape), eb=eb, block_edge=b, padding=pol,
+                radius=radius, n_out=int(s.outlier_values.size))
+    if with_blob:
+        blob = compress(data, cfg)
+        back, _ = decompress(blob)
+        arrays["blob"] = np.frombuffer(blob, dtype=np.uint8)
+        arrays["decompressed"] = back
+        # lane-1 scalar kernel must agree (criterion 2) -- recorded, not stored
+        ref = dualquant_scalar(data, _cfg(eb, b, pol, radius, lanes=1))
+        assert ref.same_bytes(s)
+    store.add(meta, **arrays)
+
+
+def make_corpus():
+    store = Store()
+    rng = np.random.default_rng(20261020)
+    caps = {1: 3000, 2: 70, 3: 18}
+    ebs = (1e-2, 1e-4, 1e-5)
+    radii = (2, 16, 512, 32768)
+    # 1) random small arrays x random configs (all decompressed by reference)
+    for i in range(60):
+        nd = i % 3 + 1
+        shape = tuple(int(round(math.exp(rng.uniform(0, math.log(caps[nd]))))) for _ in range(nd))
+        data = (_noise if i % 2 else _smooth)(rng, shape)
+        b = (8, 16, 32, 64)[int(rng.integers(0, 4))]
+        pol = POLICIES[i % len(POLICIES)]
+        eb = ebs[int(rng.integers(0, 3))]
+        radius = radii[int(rng.integers(0, 4))]
+        stream_case(store, data, eb, b, pol, radius, f"rand{i}", with_blob=data.size <= 3000)
+    # 2) edge shapes
+    edges = [(1,), (2,), (8,), (9,), (65,), (1, 1), (1, 129), (5, 1, 7), (63, 65, 9),
+             (17, 1), (1, 1, 1), (9, 9, 9), (8, 8, 8), (33, 31)]
+    for j, shape in enumerate(edges):
+        data = (_smooth if j % 2 else _noise)(rng, shape)
+        for b in (8, 64):
+            pol = POLICIES[(j + b) % len(POLICIES)]
+            stream_case(store, data, 1e-4, b, pol, 32768, f"edge{j}_b{b}",
+                        with_blob=data.size <= 3000)
+    # 3) every policy on a 3D and a 2D array with partial blocks
+    d3 = _smooth(rng, (19, 21, 23))
+    d2 = _smooth(rng, (45, 37))
+    d1 = _smooth(rng, (1000,))
+    for pol in POLICIES:
+        for b in (8, 16):
+            stream_case(store, d3, 1e-3, b, pol, 512, f"pol3d_{pol}_b{b}", with_blob=False)
+        stream_case(store, d2, 1e-4, 16, pol, 512, f"pol2d_{pol}", with_blob=True)
+        stream_case(store, d1, 1e-4, 32, pol, 64, f"pol1d_{pol}", with_blob=True)
+    # 4) larger blocks in 3D (b=32, 64) incl. outlier-heavy noise
+    stream_case(store, _smooth(rng, (64, 64, 64)), 1e-4, 32, "mean:block", 512, "big32", False)
+    stream_case(store, _noise(rng, (40, 70, 66)), 1e-4, 64, "max:edge", 32768, "big64", False)
+    stream_case(store, _noise(rng, (30, 33, 40)), 1e-5, 8, "mean:global", 512, "noise8", False)
+    stream_case(store, _noise(rng, (60, 50)), 1e-2, 32, "zero", 2, "r2", True)
+    # 5) tie-rich, narrowing-heavy and near-overflow data
+    for eb in (0.5, 2.0**-10, 1e-3):
+        stream_case(store, _ties(rng, (20, 24, 16), eb), eb, 8, "mean:global", 512,
+                    f"ties{eb}", False)
+    stream_case(store, _ties(rng, (3000,), 0.25), 0.25, 16, "zero", 32768, "ties1d", True)
+    stream_case(store, _narrow(rng, (24, 24, 24)), 1e-5, 8, "mean:global", 32768, "narrow3d", False)
+    stream_case(store, _narrow(rng, (2000,)), 1e-5, 64, "min:block", 512, "narrow1d", True)
+    stream_case(store, _big_q(rng, (16, 16, 16), 1e-3), 1e-3, 8, "zero", 32768, "bigq_zero", False)
+    stream_case(store, _big_q(rng, (16, 16, 16), 1e-3), 1e-3, 8, "mean:block", 32768, "bigq_mean", False)
+    stream_case(store, _big_q(rng, (40, 40), 1e-3), 1e-3, 16, "max:edge", 512, "bigq2d", False)
+    # 6) constant fields (acceptance criterion 4)
+    for dims in ((64,), (24, 16), (8, 8, 16)):
+        for b in (8, 16, 32, 64):
+            for pol in ("zero", "mean:global"):
+                stream_case(store, np.full(dims, 100.0, np.float32), 1e-4, b, pol, 32768,
+                            f"const{len(dims)}d_b{b}_{pol}", True)
+    # 7) BASELINE config 1 at block 256 (patched valid edges), reduced size
+    c1 = workloads.gen_c1(20000, seed=11)
+    eb1 = workloads.value_range_eb(c1, 1e-4)
+    stream_case(store, c1, eb1, 256, "zero", 512, "c1small_b256", True)
+    stream_case(store, c1, eb1, 64, "zero", 512, "c1small_b64", True)
+    store.save("corpus.npz")
+
+
+def _exc(fn):
+    try:
+        fn()
+    except verr.VlzError as exc:
+        d = {"type": type(exc).__name__, "message": str(exc)}
+        if isinstance(exc, verr.BoundTooSmallError):
+            d.update(index=exc.index, value=exc.value, bound=exc.bound)
+        return d
+    return None
+
+
+def make_errors():
+    cases = []
+
+    def add(tag, data, eb, b=8, pol="mean:global"):
+        res = _exc(lambda: dualquant_vector(data, _cfg(eb, b, pol, 32768)))
+        cases.append(dict(tag=tag, data=data.tolist(), shape=list(data.shape), eb=eb,
+                          block_edge=b, padding=pol, expect=res))
+
+    add("overflow_index", np.array([1.0, 3e5, 1.0], np.float32), 1e-5)
+    add("nan", np.array([1.0, np.nan], np.float32), 1e-4)
+    add("inf_after_overflow", np.array([3e5, 1.0, np.inf, 2.0], np.float32), 1e-5)
+    add("overflow_2d", np.array([[0.0, 1.0], [5e9, -5e9]], np.float32), 1.0)
+    add("overflow_exact_limit", np.array([0.0, float(np.float32(2**31 - 1))], np.float32), 0.5)
+    add("below_limit", np.array([0.0, float(np.float32(2**31 - 256))], np.float32), 0.5)
+    add("neg_inf_3d", np.full((2, 3, 4), 1.0, np.float32) * np.array([1, 1, 1, -np.inf], np.float32), 0.1)
+    add("ok_tiny", np.array([1e-38, -1e-45, 0.0], np.float32), 1e-4)
+    # relative bound on constant data -> DegenerateRangeError
+    const = np.full((10,), 3.0, np.float32)
+    res = _exc(lambda: dualquant_vector(const, CompressionConfig(ErrorBound.relative(1e-3))))
+    cases.append(dict(tag="degenerate_rel", data=const.tolist(), shape=[10], eb=None, rel=1e-3,
+                      block_edge=16, padding="mean:global", expect=res))
+    with open(os.path.join(HERE, "errors.json"), "w") as fh:
+        json.dump(cases, fh, indent=1)
+    print(f"wrote errors.json: {len(cases)} cases")
+
+
+def make_corrupt():
+    """reconstruct_block / decompress_parsed error cases on tampered streams."""
+    store = Store()
+    rng = np.random.default_rng(5)
+    data = _smooth(rng, (20, 13))
+    data[rng.random(data.shape) < 0.08] = 500.0  # spikes -> a few outliers per block
+    cfg = _cfg(1e-4, 8, "mean:block", 32768)
+    blob = compress(data, cfg)
+    parsed = deserialize(blob)
+    from vlz.huffman import decode
+
+    codes = decode(parsed.code_bits, parsed.code_bit_length, parsed.codebook,
+                   parsed.descriptor.element_count)
+    from vlz.model import build_block_grid
+    from vlz.padding import apply_padding
+
+    grid = build_block_grid(parsed.descriptor, 8)
+
+    def run_blocks(codes, ovals, counts):
+        # decompress_parsed semantics minus Huffman (reconstruct.py:87-124)
+        n_sentinel = int(np.count_nonzero(codes == 0))
+        if n_sentinel != len(ovals):
+            raise verr.CorruptStreamError(f"{n_sentinel} sentinel codes but {len(ovals)} outliers")
+        sizes = np.array([int(np.prod(grid.block_extents(b))) for b in range(grid.block_count)])
+        cs = np.concatenate([[0], np.cumsum(sizes)])
+        os_ = np.concatenate([[0], np.cumsum(counts)])
+        for bi in range(grid.block_count):
+            reconstruct_block(codes[cs[bi]:cs[bi + 1]], ovals[os_[bi]:os_[bi + 1]],
+                              apply_padding(parsed.scalars, grid, bi), grid.block_extents(bi),
+                              parsed.resolved_abs, parsed.radius)
+
+    variants = []
+    c = codes.copy(); c[np.flatnonzero(c != 0)[3]] = 2 * parsed.radius  # code out of range
+    variants.append(("code_range", c, parsed.outlier_values, parsed.outlier_counts))
+    c = codes.copy(); idx = np.flatnonzero(c != 0)[70]; c[idx] = 0  # extra sentinel
+    variants.append(("sentinel_total", c, parsed.outlier_values, parsed.outlier_counts))
+    cnt = parsed.outlier_counts.copy()
+    nz = np.flatnonzero(cnt)
+    cnt[nz[0]] -= 1; cnt[nz[1]] += 1  # per-block partition wrong
+    variants.append(("partition", codes, parsed.outlier_values, cnt))
+    cnt = parsed.outlier_counts.copy(); cnt[nz[0]] += 1; cnt[nz[-1]] -= 1
+    variants.append(("partition_rev", codes, parsed.outlier_values, cnt))
+    for tag, c, ov, cnt in variants:
+        res = _exc(lambda: run_blocks(c, ov, cnt))
+        store.add(dict(tag=tag, shape=list(data.shape), eb=parsed.resolved_abs, block_edge=8,
+                       padding="mean:block", radius=parsed.radius, expect=res),
+                  codes=c.astype(np.uint32), outlier_values=ov, outlier_counts=cnt,
+                  scalars=parsed.padding_values)
+    store.save("corrupt.npz")
+
+
+def make_known():
+    from vlz.quantize import prequantize
+
+    cases = []
+    for v, eb in ((3.2, 0.5), (-0.00015, 1e-4), (2.5, 0.5), (-2.5, 0.5), (0.0, 1.0),
+                  (-0.0, 1.0), (1e-45, 1e-3), (1.5, 0.5), (0.49999997, 0.5)):
+        arr = np.array([v], np.float32)
+        cases.append(dict(kind="prequant", v=float(arr[0]), eb=eb,
+                          d=int(prequantize(arr, eb).values[0])))
+    # random prequant known answers incl. ties
+    rng = np.random.default_rng(17)
+    vals = np.concatenate([rng.uniform(-1e3, 1e3, 500), (np.arange(-50, 50) + 0.5) * 0.002])
+    vals = vals.astype(np.float32)
+    for eb in (1e-2, 1e-3, 1e-4, 1e-5):
+        q = prequantize(vals, eb).values
+        cases.append(dict(kind="prequant_vec", eb=eb, v=vals.tolist(), d=q.tolist()))
+    with open(os.path.join(HERE, "known.json"), "w") as fh:
+        json.dump(cases, fh)
+    print(f"wrote known.json: {len(cases)} cases")
+
+
+def _sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def make_fullsize():
+    out = []
+    c1 = workloads.gen_c1()
+    eb1 = workloads.value_range_eb(c1, 1e-4)
+    c2 = workloads.gen_c2()
+    eb2 = workloads.value_range_eb(c2, 1e-4)
+    runs = [("C1", c1, eb1, 256, "zero"), ("C1", c1, eb1, 64, "zero"),
+            ("C2", c2, eb2, 16, "zero"), ("C2", c2, eb2, 16, "mean:block")]
+    for name, data, eb, b, pol in runs:
+        s = dualquant_vector(data, _cfg(eb, b, pol, 512, lanes=16))
+        out.append(dict(config=name, eb=eb, block_edge=b, padding=pol, radius=512,
+                        data_sha=_sha(data),
+                        codes_u16_sha=_sha(s.codes.astype(np.uint16)),
+                        outliers_sha=_sha(s.outlier_values), counts_sha=_sha(s.outlier_counts),
+                        scalars_sha=_sha(s.scalars.values), n_out=int(s.outlier_values.size)))
+        print(name, b, pol, "outliers", out[-1]["n_out"])
+    with open(os.path.join(HERE, "fullsize.json"), "w") as fh:
+        json.dump(out, fh, indent=1)
+    print("wrote fullsize.json")
+
+
+if __name__ == "__main__":
+    what = sys.argv[1:] or ["corpus", "errors", "corrupt", "known", "fullsize"]
+    for w in what:
+        globals()[f"make_{w}"]()
