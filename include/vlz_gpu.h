@@ -1,0 +1,173 @@
+/*
+ * vlz_gpu.h -- C ABI of the B200-native dual-quantization path.
+ *
+ * Drop-in boundary for the reference package `vlz` (Python, numpy).  The
+ * reference has no FFI of its own; its seams are Python functions, so each
+ * entry point below names the reference function it replaces (paths relative
+ * to /root/reference/pkg/src/vlz/).  INTEGRATION.md shows the ctypes binding a
+ * maintainer adds on the reference side.
+ *
+ * Conventions
+ *  - plain pointers + sizes, no torch types; every `d_*` pointer is device
+ *    memory, every `h_*` pointer is host memory (pinned for full speed).
+ *  - `stream` is a cudaStream_t passed as void* (0 = legacy default stream).
+ *  - all device entry points are asynchronous and stream-ordered; errors found
+ *    on the device (non-finite input, quantizer overflow, corrupt streams) are
+ *    reported in a caller-allocated device `vlz_result` the caller reads back.
+ *  - return value: VLZ_OK or a launch/argument error (VLZ_E_ARG, VLZ_E_CUDA).
+ *  - the library allocates nothing on the device paths (workspace is caller
+ *    owned); the *_host paths keep a per-device cache of staging buffers.
+ */
+#ifndef VLZ_GPU_H_
+#define VLZ_GPU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* return codes of the entry points */
+#define VLZ_OK 0
+#define VLZ_E_ARG 1  /* invalid geometry / parameters (host-side check) */
+#define VLZ_E_CUDA 2 /* CUDA launch / memory error                      */
+
+/* device-side status codes (vlz_result.status).  Mapped by the Python layer
+ * onto the reference's exception classes (errors.py:8-62):               */
+#define VLZ_ST_OK 0
+#define VLZ_ST_NONFINITE 1       /* ConfigError: non-finite value at flat index   */
+#define VLZ_ST_OVERFLOW 2        /* BoundTooSmallError(index, value, eb)          */
+#define VLZ_ST_CORRUPT_CODE 4    /* CorruptStreamError: code >= 2R (first block)  */
+#define VLZ_ST_EXHAUSTED 5       /* CorruptStreamError: outliers exhausted        */
+#define VLZ_ST_LEFTOVER 6        /* CorruptStreamError: leftover outliers         */
+#define VLZ_ST_SENTINEL_TOTAL 7  /* CorruptStreamError: sentinels != outliers     */
+
+/* padding policy codes: container.py:57-58 ordering */
+#define VLZ_PAD_ZERO 0
+#define VLZ_PAD_MIN 1
+#define VLZ_PAD_MAX 2
+#define VLZ_PAD_MEAN 3
+#define VLZ_GRAN_GLOBAL 0
+#define VLZ_GRAN_BLOCK 1
+#define VLZ_GRAN_EDGE 2
+
+/* Array geometry + block tiling (model.py:48-159).  dims are the reference's
+ * row-major extents, dims[0] slowest; only the first nd entries are read. */
+typedef struct vlz_geom {
+  int32_t nd;         /* 1, 2 or 3                                         */
+  int32_t block_edge; /* 8, 16, 32, 64 (256 accepted for nd == 1)          */
+  int64_t dims[3];
+} vlz_geom;
+
+/* Quantizer parameters (model.py:200-231, padding policy model.py:162-197) */
+typedef struct vlz_params {
+  double eb;          /* resolved absolute error bound (model.py:94-110)  */
+  int32_t radius;     /* 2 .. 32768                                        */
+  int32_t pad_kind;   /* VLZ_PAD_*                                         */
+  int32_t pad_gran;   /* VLZ_GRAN_*                                        */
+  int32_t reserved;
+} vlz_params;
+
+/* Device-written result block (64 bytes). */
+typedef struct vlz_result {
+  int32_t status;        /* VLZ_ST_*                                          */
+  int32_t reserved;
+  int64_t index;         /* flat element index (compress) / block index      */
+  int64_t n_outliers;    /* compress: outliers written; decompress: sentinels */
+  int64_t first_nonfinite; /* raw minima, INT64_MAX when none                */
+  int64_t first_overflow;
+  int64_t first_bad_block; /* (block << 4) | status, INT64_MAX when none     */
+  int64_t sentinels;
+  int64_t pad0;
+} vlz_result;
+
+/* Global padding statistics over the prequantized field (padding.py:62-69),
+ * accumulated by compress_begin; all-reduced across ranks for sharded runs
+ * (sum: wrapping int64 add; count: add; min: min; neg_max: min of -max). */
+typedef struct vlz_stats {
+  int64_t sum;
+  int64_t count;
+  int64_t min;
+  int64_t neg_max;
+} vlz_stats;
+
+/* ---- geometry helpers (host) --------------------------------------- */
+int64_t vlz_block_count(const vlz_geom* g);
+/* PaddingPolicy.scalar_count (model.py:167-175) */
+int64_t vlz_scalar_count(const vlz_geom* g, int32_t pad_kind, int32_t pad_gran);
+/* Device workspace bytes needed by compress/decompress for this geometry. */
+size_t vlz_workspace_size(const vlz_geom* g);
+
+/* ---- compress: replaces vector.dualquant_vector (vector.py:205-260) ---- *
+ * d_in         float32[N] row-major input
+ * d_codes      uint16[N] quantization codes, canonical block-major order
+ *              (0 = outlier sentinel; CodeStream.codes, model.py:254)
+ * d_outliers   float32[N] capacity; the first n_outliers hold the verbatim
+ *              outlier values in canonical order (CodeStream.outlier_values)
+ * d_counts     int64[nblocks] outliers per block (CodeStream.outlier_counts)
+ * d_scalars    int64[scalar_count] padding scalars (PaddingScalars.values)
+ * d_result     status, first error indices and n_outliers                    */
+int vlz_dq_compress(const float* d_in, const vlz_geom* g, const vlz_params* p,
+                    uint16_t* d_codes, float* d_outliers, int64_t* d_counts,
+                    int64_t* d_scalars, vlz_result* d_result, void* d_ws,
+                    size_t ws_bytes, void* stream);
+
+/* Two-phase form for slab-sharded multi-GPU runs (each rank compresses a
+ * block-aligned slab along dims[0]).  begin = fused prequant + Lorenzo +
+ * postquant + block/edge padding; for *:global policies it also writes this
+ * shard's partial statistics to d_stats and leaves block origins pending.
+ * The caller all-reduces d_stats (NCCL) and then calls finish, which resolves
+ * the global scalar, the origin codes and compacts the outliers. */
+int vlz_dq_compress_begin(const float* d_in, const vlz_geom* g, const vlz_params* p,
+                          uint16_t* d_codes, int64_t* d_counts, int64_t* d_scalars,
+                          vlz_result* d_result, vlz_stats* d_stats, void* d_ws,
+                          size_t ws_bytes, void* stream);
+int vlz_dq_compress_finish(const float* d_in, const vlz_geom* g, const vlz_params* p,
+                           const vlz_stats* d_global_stats, uint16_t* d_codes,
+                           float* d_outliers, int64_t* d_counts, int64_t* d_scalars,
+                           vlz_result* d_result, void* d_ws, size_t ws_bytes, void* stream);
+
+/* ---- decompress: replaces reconstruct.decompress_parsed minus the Huffman
+ * decode (reconstruct.py:30-124).  Codes uint16 (container symbol width) or
+ * uint32 (CodeStream width).  d_out float32[N] row-major.  Stream corruption
+ * is reported in d_result (status, index = first failing block). ---------- */
+int vlz_dq_decompress(const uint16_t* d_codes, const float* d_outliers,
+                      int64_t n_outliers, const int64_t* d_counts, const int64_t* d_scalars,
+                      const vlz_geom* g, const vlz_params* p, float* d_out,
+                      vlz_result* d_result, void* d_ws, size_t ws_bytes, void* stream);
+int vlz_dq_decompress_u32(const uint32_t* d_codes, const float* d_outliers,
+                          int64_t n_outliers, const int64_t* d_counts,
+                          const int64_t* d_scalars, const vlz_geom* g, const vlz_params* p,
+                          float* d_out, vlz_result* d_result, void* d_ws, size_t ws_bytes,
+                          void* stream);
+
+/* ---- value range for ErrorBound.relative (model.py:104-110) ------------ *
+ * d_minmax[0] = float(min), d_minmax[1] = float(max), NaN-propagating like
+ * numpy's min/max. */
+int vlz_minmax(const float* d_in, int64_t n, double* d_minmax, void* stream);
+
+/* ---- host-buffer entry points (end-to-end: H2D + kernels + D2H) -------- *
+ * Same semantics as the device versions; buffers are host memory (pinned for
+ * full PCIe speed).  Synchronous: returns after the results are in host
+ * memory.  *h_result receives the status block. */
+int vlz_dq_compress_host(const float* h_in, const vlz_geom* g, const vlz_params* p,
+                         uint16_t* h_codes, float* h_outliers, int64_t* h_counts,
+                         int64_t* h_scalars, vlz_result* h_result, int device);
+int vlz_dq_decompress_host(const uint16_t* h_codes, const float* h_outliers,
+                           int64_t n_outliers, const int64_t* h_counts,
+                           const int64_t* h_scalars, const vlz_geom* g, const vlz_params* p,
+                           float* h_out, vlz_result* h_result, int device);
+/* release the cached staging buffers of the host entry points */
+void vlz_host_release(void);
+
+/* number of kernel launches the library issued since load (bench evidence) */
+int64_t vlz_launch_count(void);
+/* library build string (arch, commit) */
+const char* vlz_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VLZ_GPU_H_ */

@@ -1,0 +1,215 @@
+// dq_scan.cuh -- single-pass block-count scan + outlier compaction.
+//
+// Turns the per-block outlier counts (CodeStream.outlier_counts, model.py:
+// 253-256) into canonical offsets with a decoupled look-back scan over chunks
+// of CH blocks (chunk order = dynamic ticket order, so every chunk only waits
+// on chunks that are already running), then copies each block's outliers from
+// its block-relative scratch slots into the compact canonical array
+// (vector.py:193-202: outliers in block-major, in-block traversal order).
+//
+// For *:global padding it first resolves the block origins that the fused
+// kernel left pending (the origin is the only element whose delta depends on
+// the global scalar): it derives s0 from the reduced
+// statistics (padding.py:62-69, 72-85), re-quantizes the origin value, writes
+// the origin code, and adds the origin to the block's count when it is an
+// outlier (its value goes to scratch slot 0).
+//
+// In OFFSETS mode (decompression) it only writes the exclusive offsets.
+#pragma once
+
+#include <cuda/atomic>
+
+#include "vlz_common.cuh"
+
+namespace vlz {
+
+constexpr int SCAN_THREADS = 256;
+constexpr int SCAN_IPT = 8;
+constexpr int SCAN_CH = SCAN_THREADS * SCAN_IPT;
+
+struct ScanArgs {
+  Geo g;
+  QP q;
+  int BZ, BY, BX;
+  int fix_origin;  // 1: resolve pending origins (*:global policies)
+  int gather;      // 1: compact outliers; 0: write offsets
+  const float* in;
+  uint16_t* codes;
+  int64_t* counts;
+  float* scratch;
+  float* out;
+  int64_t* offsets;
+  int64_t* scalars;
+  unsigned long long* lb;  // per chunk look-back words
+  unsigned int* ticket;
+  long long* n_out;
+  const long long* gstats;  // sum, count, min, neg_max (reduced)
+  // compress status finalisation (done by the chunk holding the last block)
+  int* status;
+  long long* index;
+  const unsigned long long* first_nonfinite;
+  const unsigned long long* first_overflow;
+};
+
+__device__ __forceinline__ void block_of(const Geo& g, int64_t bi, int BZ, int BY, int BX,
+                                         int64_t& bstart, int64_t& origin) {
+  const int64_t bx = bi % g.P2;
+  const int64_t t = bi / g.P2;
+  const int64_t by = t % g.P1;
+  const int64_t bz = t / g.P1;
+  const int64_t ez = imin64(BZ, g.D0 - bz * BZ);
+  const int64_t ey = imin64(BY, g.D1 - by * BY);
+  bstart = block_start(g, bz, by, bx, BZ, BY, BX, ez, ey);
+  origin = ((bz * BZ) * g.D1 + by * BY) * g.D2 + bx * BX;
+}
+
+constexpr unsigned long long FLAG_A = 1ull << 62;
+constexpr unsigned long long FLAG_P = 2ull << 62;
+constexpr unsigned long long VAL_MASK = (1ull << 62) - 1;
+
+__global__ void __launch_bounds__(SCAN_THREADS) dq_scan_kernel(ScanArgs a) {
+  __shared__ long long s_inc[SCAN_CH];   // chunk-local inclusive prefix per block
+  __shared__ long long s_src[SCAN_CH];   // scratch source of each block's outliers
+  __shared__ long long s_warp[SCAN_THREADS / 32];
+  __shared__ long long s_excl;
+  __shared__ unsigned int s_tile;
+
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) s_tile = atomicAdd(a.ticket, 1u);
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const int64_t base = tile * SCAN_CH;
+  const int64_t nb = a.g.nblocks;
+
+  int64_t s0 = 0;
+  if (a.fix_origin) {
+    const long long* gs = a.gstats;
+    s0 = stat_value(a.q.kind, gs[0], gs[1], gs[2], -gs[3]);
+  }
+
+  long long c[SCAN_IPT];
+  long long tsum = 0;
+#pragma unroll
+  for (int k = 0; k < SCAN_IPT; ++k) {
+    const int64_t bi = base + (int64_t)tid * SCAN_IPT + k;
+    c[k] = 0;
+    if (bi < nb) {
+      c[k] = a.counts[bi];
+      if (a.fix_origin || (a.gather && c[k] > 0)) {
+        int64_t bstart, origin;
+        block_of(a.g, bi, a.BZ, a.BY, a.BX, bstart, origin);
+        if (a.fix_origin) {
+          bool bad, ovf;
+          const float v = a.in[origin];
+          const int d = quant_exact(v, a.q, bad, ovf);
+          const int64_t delta = (int64_t)d - s0;
+          const int R = a.q.radius;
+          const bool out = bad || delta > (int64_t)(R - 1) || delta < -(int64_t)(R - 1);
+          a.codes[bstart] = out ? (uint16_t)0 : (uint16_t)(delta + R);
+          if (out) {
+            a.scratch[bstart] = v;
+            c[k] += 1;
+          }
+          a.counts[bi] = c[k];
+          s_src[tid * SCAN_IPT + k] = bstart + (out ? 0 : 1);
+        } else {
+          s_src[tid * SCAN_IPT + k] = bstart + (a.codes[bstart] == 0 ? 0 : 1);
+        }
+      }
+    }
+    tsum += c[k];
+  }
+  // block-wide exclusive scan of the per-thread sums
+  long long inc = tsum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long u = __shfl_up_sync(FULL, inc, o);
+    if (lane >= o) inc += u;
+  }
+  if (lane == 31) s_warp[wid] = inc;
+  __syncthreads();
+  long long wbase = 0, agg = 0;
+#pragma unroll
+  for (int w = 0; w < SCAN_THREADS / 32; ++w) {
+    if (w < wid) wbase += s_warp[w];
+    agg += s_warp[w];
+  }
+  const long long texcl = wbase + inc - tsum;
+
+  // decoupled look-back (warp 0)
+  if (wid == 0) {
+    cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> me(a.lb[tile]);
+    if (lane == 0) me.store((tile == 0 ? FLAG_P : FLAG_A) | (unsigned long long)agg,
+                            cuda::memory_order_relaxed);
+    long long excl = 0;
+    int64_t pred = tile - 1;
+    while (pred >= 0) {
+      const int64_t idx = pred - lane;
+      unsigned long long w = FLAG_P;
+      if (idx >= 0) {
+        cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> r(a.lb[idx]);
+        w = r.load(cuda::memory_order_relaxed);
+        while ((w >> 62) == 0) w = r.load(cuda::memory_order_relaxed);
+      }
+      const unsigned pm = __ballot_sync(FULL, (w >> 62) == 2);
+      const int stop = pm ? __ffs(pm) - 1 : 31;
+      long long val = (lane <= stop) ? (long long)(w & VAL_MASK) : 0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(FULL, val, o);
+      excl += val;
+      if (pm) break;
+      pred -= 32;
+    }
+    if (lane == 0) {
+      if (tile > 0) me.store(FLAG_P | (unsigned long long)(excl + agg), cuda::memory_order_relaxed);
+      s_excl = excl;
+      if (base + SCAN_CH >= nb) {
+        *a.n_out = excl + agg;
+        if (a.fix_origin && a.scalars) a.scalars[0] = s0;
+        if (a.status) {
+          // quantize.py:62-72 precedence: any non-finite value first, then overflow
+          const unsigned long long nf = *a.first_nonfinite, ov = *a.first_overflow;
+          if (nf != 0x7fffffffffffffffull) {
+            *a.status = 1;  // VLZ_ST_NONFINITE
+            *a.index = (long long)nf;
+          } else if (ov != 0x7fffffffffffffffull) {
+            *a.status = 2;  // VLZ_ST_OVERFLOW
+            *a.index = (long long)ov;
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  const long long cexcl = s_excl;
+
+  // per-block offsets
+  long long run = texcl;
+#pragma unroll
+  for (int k = 0; k < SCAN_IPT; ++k) {
+    const int64_t bi = base + (int64_t)tid * SCAN_IPT + k;
+    if (!a.gather) {
+      if (bi < nb) a.offsets[bi] = cexcl + run;
+    }
+    run += c[k];
+    s_inc[tid * SCAN_IPT + k] = run;
+  }
+  if (!a.gather) return;
+  __syncthreads();
+
+  // cooperative gather of this chunk's outliers
+  const long long T = agg;
+  for (long long t = tid; t < T; t += SCAN_THREADS) {
+    // first k with s_inc[k] > t
+    int lo = 0, hi = SCAN_CH - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (s_inc[mid] > t) hi = mid;
+      else lo = mid + 1;
+    }
+    const long long kexcl = lo ? s_inc[lo - 1] : 0;
+    a.out[cexcl + t] = a.scratch[s_src[lo] + (t - kexcl)];
+  }
+}
+
+}  // namespace vlz

@@ -1,0 +1,51 @@
+// launch.cuh -- host-side launch helpers shared by the kernel translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+
+#include "dq_decompress.cuh"
+
+namespace vlz {
+
+// total kernel launches issued by the library (evidence for bench.py)
+extern std::atomic<long long> g_launches;
+
+int num_sms();
+
+// grid = min(resident CTAs, tiles/4) for a 128-thread warp-per-tile kernel
+template <typename Kern, typename Arg>
+inline cudaError_t launch_tiles(Kern kernel, int64_t ntiles, int smem, cudaStream_t st,
+                                const Arg& arg) {
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+  }
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 128, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  int64_t grid = (int64_t)per_sm * num_sms();
+  const int64_t need = (ntiles + 3) / 4;
+  if (grid > need) grid = need;
+  if (grid < 1) grid = 1;
+  kernel<<<(unsigned)grid, 128, smem, st>>>(arg);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+// per-(nd) dispatch entry points, one translation unit each
+cudaError_t launch_compress_nd1(int B, int mode, const CompressArgs& a, cudaStream_t st);
+cudaError_t launch_compress_nd2(int B, int mode, const CompressArgs& a, cudaStream_t st);
+cudaError_t launch_compress_nd3(int B, int mode, const CompressArgs& a, cudaStream_t st);
+cudaError_t launch_decompress(int nd, int B, bool u32, const DecompressArgs& a, cudaStream_t st);
+
+// window width (columns per warp tile) used for (nd, B)
+inline int vpl_for(int nd, int B) {
+  if (nd == 1 && B == 256) return 8;
+  if (nd == 3 && B == 64) return 2;
+  return 4;
+}
+
+}  // namespace vlz

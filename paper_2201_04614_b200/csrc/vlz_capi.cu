@@ -1,0 +1,593 @@
+// vlz_capi.cu -- the C ABI declared in include/vlz_gpu.h.
+//
+// Host orchestration only: argument validation (model.py:48-231 rules),
+// workspace carving, and the launch sequence
+//   compress   : init -> fused K1 (dq_compress) -> scan/origin-fix/gather
+//   decompress : init -> scan (offsets) -> fused K4 (dq_decompress)
+// Every kernel is stream-ordered on the caller's stream; nothing synchronises
+// except the *_host entry points, which stage through cached device buffers.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "../../include/vlz_gpu.h"
+#include "dq_scan.cuh"
+#include "launch.cuh"
+
+namespace vlz {
+
+std::atomic<long long> g_launches{0};
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+namespace {
+
+constexpr unsigned long long I64MAX = 0x7fffffffffffffffull;
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+bool valid_geom(const vlz_geom* g) {
+  if (!g || g->nd < 1 || g->nd > 3) return false;
+  const int b = g->block_edge;
+  const bool b_ok = b == 8 || b == 16 || b == 32 || b == 64 || (b == 256 && g->nd == 1);
+  if (!b_ok) return false;
+  for (int d = 0; d < g->nd; ++d)
+    if (g->dims[d] < 1) return false;
+  return true;
+}
+
+bool make_geo(const vlz_geom* gg, Geo& g) {
+  if (!valid_geom(gg)) return false;
+  const int b = gg->block_edge;
+  int64_t D[3] = {1, 1, 1};
+  for (int d = 0; d < gg->nd; ++d) D[3 - gg->nd + d] = gg->dims[d];
+  const int BZ = gg->nd == 3 ? b : 1, BY = gg->nd >= 2 ? b : 1, BX = b;
+  g.D0 = D[0];
+  g.D1 = D[1];
+  g.D2 = D[2];
+  g.P0 = (D[0] + BZ - 1) / BZ;
+  g.P1 = (D[1] + BY - 1) / BY;
+  g.P2 = (D[2] + BX - 1) / BX;
+  const int W = 32 * vpl_for(gg->nd, b);
+  g.NW = (D[2] + W - 1) / W;
+  g.ntiles = g.P0 * g.P1 * g.NW;
+  g.nblocks = g.P0 * g.P1 * g.P2;
+  g.N = D[0] * D[1] * D[2];
+  return true;
+}
+
+int mode_of(int kind, int gran) {
+  if (kind == VLZ_PAD_ZERO) return MODE_ZERO;
+  if (gran == VLZ_GRAN_GLOBAL) return MODE_GLOBAL;
+  if (gran == VLZ_GRAN_BLOCK) return MODE_BLOCK;
+  return MODE_EDGE;
+}
+
+bool valid_params(const vlz_params* p) {
+  if (!p) return false;
+  if (p->radius < 2 || p->radius > 32768) return false;
+  if (p->pad_kind < 0 || p->pad_kind > 3 || p->pad_gran < 0 || p->pad_gran > 2) return false;
+  return true;
+}
+
+// workspace layout
+struct WS {
+  unsigned int* ticket;      // scan chunk ticket
+  unsigned int* done;        // finished-CTA counter
+  long long* stats;          // sum, count, min, neg_max (single-GPU compress)
+  long long* aux;            // 8 spare words
+  unsigned long long* lb;    // look-back words, one per scan chunk
+  int64_t* offsets;          // nblocks
+  float* scratch;            // N
+  size_t bytes;
+};
+
+WS carve(const Geo& g, void* base) {
+  WS w{};
+  char* p = static_cast<char*>(base);
+  size_t off = 0;
+  w.ticket = reinterpret_cast<unsigned int*>(p + off);
+  w.done = reinterpret_cast<unsigned int*>(p + off + 8);
+  w.stats = reinterpret_cast<long long*>(p + off + 64);
+  w.aux = reinterpret_cast<long long*>(p + off + 128);
+  off += 256;
+  const int64_t nchunks = (g.nblocks + SCAN_CH - 1) / SCAN_CH;
+  w.lb = reinterpret_cast<unsigned long long*>(p + off);
+  off += align256((size_t)nchunks * 8);
+  w.offsets = reinterpret_cast<int64_t*>(p + off);
+  off += align256((size_t)g.nblocks * 8);
+  w.scratch = reinterpret_cast<float*>(p + off);
+  off += align256((size_t)g.N * 4);
+  w.bytes = off;
+  return w;
+}
+
+// one tiny kernel resets the result block, the counters and look-back words
+__global__ void init_kernel(vlz_result* res, unsigned int* ticket, unsigned int* done,
+                            long long* stats, unsigned long long* lb, int64_t nchunks) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0) {
+    if (res) {
+      res->status = 0;
+      res->reserved = 0;
+      res->index = -1;
+      res->n_outliers = 0;
+      res->first_nonfinite = (int64_t)I64MAX;
+      res->first_overflow = (int64_t)I64MAX;
+      res->first_bad_block = (int64_t)I64MAX;
+      res->sentinels = 0;
+      res->pad0 = 0;
+    }
+    *ticket = 0;
+    *done = 0;
+    if (stats) {
+      stats[0] = 0;
+      stats[1] = 0;
+      stats[2] = (long long)I64MAX;
+      stats[3] = (long long)I64MAX;
+    }
+  }
+  for (int64_t k = i; k < nchunks; k += (int64_t)gridDim.x * blockDim.x) lb[k] = 0;
+}
+
+cudaError_t launch_init(vlz_result* res, const WS& w, long long* stats, int64_t nchunks,
+                        cudaStream_t st) {
+  int64_t blocks = (nchunks + 255) / 256;
+  if (blocks < 1) blocks = 1;
+  if (blocks > 1024) blocks = 1024;
+  init_kernel<<<(unsigned)blocks, 256, 0, st>>>(res, w.ticket, w.done, stats, w.lb, nchunks);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scan(const ScanArgs& a, cudaStream_t st) {
+  int64_t nchunks = (a.g.nblocks + SCAN_CH - 1) / SCAN_CH;
+  if (nchunks < 1) nchunks = 1;
+  dq_scan_kernel<<<(unsigned)nchunks, SCAN_THREADS, 0, st>>>(a);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+int to_rc(cudaError_t e) {
+  if (e == cudaSuccess) return VLZ_OK;
+  std::fprintf(stderr, "vlz_gpu: CUDA error %s\n", cudaGetErrorString(e));
+  return VLZ_E_CUDA;
+}
+
+QP make_qp(const vlz_params* p) {
+  QP q;
+  q.eb = p->eb;
+  q.twoeb = 2.0 * p->eb;
+  q.radius = p->radius;
+  q.kind = p->pad_kind;
+  return q;
+}
+
+// ---- value range (ErrorBound.relative) -------------------------------
+__device__ __forceinline__ unsigned fkey(float f) {
+  const unsigned u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float fkey_inv(unsigned k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+
+__global__ void minmax_kernel(const float* in, int64_t n, unsigned int* kmin, unsigned int* kmax,
+                              unsigned int* nan, unsigned int* done, double* out) {
+  unsigned lo = 0xffffffffu, hi = 0u, isnan = 0u;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = in[i];
+    if (v != v) {
+      isnan = 1u;
+    } else {
+      const unsigned k = fkey(v);
+      lo = k < lo ? k : lo;
+      hi = k > hi ? k : hi;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned a = __shfl_xor_sync(FULL, lo, o), b = __shfl_xor_sync(FULL, hi, o);
+    lo = a < lo ? a : lo;
+    hi = b > hi ? b : hi;
+    isnan |= __shfl_xor_sync(FULL, isnan, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(kmin, lo);
+    atomicMax(kmax, hi);
+    if (isnan) atomicOr(nan, 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(done, 1u) == gridDim.x - 1) {
+      __threadfence();
+      const unsigned a = atomicAdd(kmin, 0u), b = atomicAdd(kmax, 0u), c = atomicAdd(nan, 0u);
+      if (c) {
+        out[0] = __longlong_as_double(0x7ff8000000000000ll);
+        out[1] = out[0];
+      } else {
+        out[0] = (double)fkey_inv(a);
+        out[1] = (double)fkey_inv(b);
+      }
+    }
+  }
+}
+
+__global__ void minmax_init(unsigned int* w) {
+  w[0] = 0xffffffffu;
+  w[1] = 0u;
+  w[2] = 0u;
+  w[3] = 0u;
+}
+
+}  // namespace
+}  // namespace vlz
+
+using namespace vlz;
+
+extern "C" {
+
+int64_t vlz_block_count(const vlz_geom* gg) {
+  Geo g;
+  if (!make_geo(gg, g)) return -1;
+  return g.nblocks;
+}
+
+int64_t vlz_scalar_count(const vlz_geom* gg, int32_t kind, int32_t gran) {
+  Geo g;
+  if (!make_geo(gg, g)) return -1;
+  if (kind == VLZ_PAD_ZERO) return 0;
+  if (gran == VLZ_GRAN_GLOBAL) return 1;
+  if (gran == VLZ_GRAN_BLOCK) return g.nblocks;
+  return g.nblocks * gg->nd;
+}
+
+size_t vlz_workspace_size(const vlz_geom* gg) {
+  Geo g;
+  if (!make_geo(gg, g)) return 0;
+  char* null_base = nullptr;
+  return carve(g, null_base).bytes;
+}
+
+static int compress_begin_impl(const float* d_in, const vlz_geom* gg, const vlz_params* p,
+                               uint16_t* d_codes, int64_t* d_counts, int64_t* d_scalars,
+                               vlz_result* d_result, long long* stats, void* d_ws,
+                               size_t ws_bytes, cudaStream_t st) {
+  Geo g;
+  if (!make_geo(gg, g) || !valid_params(p) || !(p->eb > 0.0) || !d_in || !d_codes ||
+      !d_counts || !d_result || !d_ws)
+    return VLZ_E_ARG;
+  WS w = carve(g, d_ws);
+  if (ws_bytes < w.bytes) return VLZ_E_ARG;
+  const int mode = mode_of(p->pad_kind, p->pad_gran);
+  if (mode != MODE_ZERO && !d_scalars) return VLZ_E_ARG;
+  if (mode == MODE_GLOBAL && !stats) return VLZ_E_ARG;
+  const int64_t nchunks = (g.nblocks + SCAN_CH - 1) / SCAN_CH;
+  cudaError_t e = launch_init(d_result, w, stats, nchunks, st);
+  if (e != cudaSuccess) return to_rc(e);
+  CompressArgs a{};
+  a.g = g;
+  a.q = make_qp(p);
+  a.in = d_in;
+  a.codes = d_codes;
+  a.scratch = w.scratch;
+  a.counts = d_counts;
+  a.scalars = d_scalars;
+  a.first_nonfinite = reinterpret_cast<unsigned long long*>(&d_result->first_nonfinite);
+  a.first_overflow = reinterpret_cast<unsigned long long*>(&d_result->first_overflow);
+  a.gsum = reinterpret_cast<unsigned long long*>(stats);
+  a.gcount = reinterpret_cast<unsigned long long*>(stats ? stats + 1 : nullptr);
+  a.gmin = stats ? stats + 2 : nullptr;
+  a.gnegmax = stats ? stats + 3 : nullptr;
+  const int b = gg->block_edge;
+  if (gg->nd == 1) e = launch_compress_nd1(b, mode, a, st);
+  else if (gg->nd == 2) e = launch_compress_nd2(b, mode, a, st);
+  else e = launch_compress_nd3(b, mode, a, st);
+  return to_rc(e);
+}
+
+static int compress_finish_impl(const float* d_in, const vlz_geom* gg, const vlz_params* p,
+                                const long long* gstats, uint16_t* d_codes, float* d_outliers,
+                                int64_t* d_counts, int64_t* d_scalars, vlz_result* d_result,
+                                void* d_ws, size_t ws_bytes, cudaStream_t st) {
+  Geo g;
+  if (!make_geo(gg, g) || !valid_params(p) || !d_outliers || !d_result || !d_ws)
+    return VLZ_E_ARG;
+  WS w = carve(g, d_ws);
+  if (ws_bytes < w.bytes) return VLZ_E_ARG;
+  const int mode = mode_of(p->pad_kind, p->pad_gran);
+  const int b = gg->block_edge;
+  ScanArgs s{};
+  s.g = g;
+  s.q = make_qp(p);
+  s.BZ = gg->nd == 3 ? b : 1;
+  s.BY = gg->nd >= 2 ? b : 1;
+  s.BX = b;
+  s.fix_origin = mode == MODE_GLOBAL;
+  s.gather = 1;
+  s.in = d_in;
+  s.codes = d_codes;
+  s.counts = d_counts;
+  s.scratch = w.scratch;
+  s.out = d_outliers;
+  s.scalars = d_scalars;
+  s.lb = w.lb;
+  s.ticket = w.ticket;
+  s.n_out = reinterpret_cast<long long*>(&d_result->n_outliers);
+  s.gstats = gstats;
+  s.status = &d_result->status;
+  s.index = reinterpret_cast<long long*>(&d_result->index);
+  s.first_nonfinite = reinterpret_cast<const unsigned long long*>(&d_result->first_nonfinite);
+  s.first_overflow = reinterpret_cast<const unsigned long long*>(&d_result->first_overflow);
+  if (mode == MODE_GLOBAL && !gstats) return VLZ_E_ARG;
+  return to_rc(launch_scan(s, st));
+}
+
+int vlz_dq_compress(const float* d_in, const vlz_geom* g, const vlz_params* p, uint16_t* d_codes,
+                    float* d_outliers, int64_t* d_counts, int64_t* d_scalars,
+                    vlz_result* d_result, void* d_ws, size_t ws_bytes, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Geo gg;
+  if (!make_geo(g, gg)) return VLZ_E_ARG;
+  WS w = carve(gg, d_ws);
+  int rc = compress_begin_impl(d_in, g, p, d_codes, d_counts, d_scalars, d_result, w.stats,
+                               d_ws, ws_bytes, st);
+  if (rc != VLZ_OK) return rc;
+  return compress_finish_impl(d_in, g, p, w.stats, d_codes, d_outliers, d_counts, d_scalars,
+                              d_result, d_ws, ws_bytes, st);
+}
+
+int vlz_dq_compress_begin(const float* d_in, const vlz_geom* g, const vlz_params* p,
+                          uint16_t* d_codes, int64_t* d_counts, int64_t* d_scalars,
+                          vlz_result* d_result, vlz_stats* d_stats, void* d_ws, size_t ws_bytes,
+                          void* stream) {
+  return compress_begin_impl(d_in, g, p, d_codes, d_counts, d_scalars, d_result,
+                             reinterpret_cast<long long*>(d_stats), d_ws, ws_bytes,
+                             static_cast<cudaStream_t>(stream));
+}
+
+int vlz_dq_compress_finish(const float* d_in, const vlz_geom* g, const vlz_params* p,
+                           const vlz_stats* d_global_stats, uint16_t* d_codes, float* d_outliers,
+                           int64_t* d_counts, int64_t* d_scalars, vlz_result* d_result,
+                           void* d_ws, size_t ws_bytes, void* stream) {
+  return compress_finish_impl(d_in, g, p, reinterpret_cast<const long long*>(d_global_stats),
+                              d_codes, d_outliers, d_counts, d_scalars, d_result, d_ws,
+                              ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
+static int decompress_impl(const void* d_codes, bool u32, const float* d_outliers,
+                           int64_t n_outliers, const int64_t* d_counts, const int64_t* d_scalars,
+                           const vlz_geom* gg, const vlz_params* p, float* d_out,
+                           vlz_result* d_result, void* d_ws, size_t ws_bytes, cudaStream_t st) {
+  Geo g;
+  if (!make_geo(gg, g) || !valid_params(p) || !d_codes || !d_counts || !d_out || !d_result ||
+      !d_ws || n_outliers < 0)
+    return VLZ_E_ARG;
+  WS w = carve(g, d_ws);
+  if (ws_bytes < w.bytes) return VLZ_E_ARG;
+  const int mode = mode_of(p->pad_kind, p->pad_gran);
+  if (mode != MODE_ZERO && !d_scalars) return VLZ_E_ARG;
+  const int64_t nchunks = (g.nblocks + SCAN_CH - 1) / SCAN_CH;
+  cudaError_t e = launch_init(d_result, w, nullptr, nchunks, st);
+  if (e != cudaSuccess) return to_rc(e);
+  const int b = gg->block_edge;
+  ScanArgs s{};
+  s.g = g;
+  s.q = make_qp(p);
+  s.BZ = gg->nd == 3 ? b : 1;
+  s.BY = gg->nd >= 2 ? b : 1;
+  s.BX = b;
+  s.fix_origin = 0;
+  s.gather = 0;
+  s.counts = const_cast<int64_t*>(d_counts);
+  s.offsets = w.offsets;
+  s.lb = w.lb;
+  s.ticket = w.ticket;
+  s.n_out = w.aux;  // sum of counts (unused by the checks; kept for debugging)
+  e = launch_scan(s, st);
+  if (e != cudaSuccess) return to_rc(e);
+  DecompressArgs a{};
+  a.g = g;
+  a.q = make_qp(p);
+  a.mode = mode;
+  a.nd = gg->nd;
+  a.codes = d_codes;
+  a.outliers = d_outliers;
+  a.n_outliers = n_outliers;
+  a.counts = d_counts;
+  a.offsets = w.offsets;
+  a.scalars = d_scalars;
+  a.out = d_out;
+  a.first_bad = reinterpret_cast<unsigned long long*>(&d_result->first_bad_block);
+  a.sentinels = reinterpret_cast<unsigned long long*>(&d_result->sentinels);
+  a.done = w.done;
+  a.status = &d_result->status;
+  a.index = reinterpret_cast<long long*>(&d_result->index);
+  a.n_sent_out = reinterpret_cast<long long*>(&d_result->n_outliers);
+  return to_rc(launch_decompress(gg->nd, b, u32, a, st));
+}
+
+int vlz_dq_decompress(const uint16_t* d_codes, const float* d_outliers, int64_t n_outliers,
+                      const int64_t* d_counts, const int64_t* d_scalars, const vlz_geom* g,
+                      const vlz_params* p, float* d_out, vlz_result* d_result, void* d_ws,
+                      size_t ws_bytes, void* stream) {
+  return decompress_impl(d_codes, false, d_outliers, n_outliers, d_counts, d_scalars, g, p, d_out,
+                         d_result, d_ws, ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int vlz_dq_decompress_u32(const uint32_t* d_codes, const float* d_outliers, int64_t n_outliers,
+                          const int64_t* d_counts, const int64_t* d_scalars, const vlz_geom* g,
+                          const vlz_params* p, float* d_out, vlz_result* d_result, void* d_ws,
+                          size_t ws_bytes, void* stream) {
+  return decompress_impl(d_codes, true, d_outliers, n_outliers, d_counts, d_scalars, g, p, d_out,
+                         d_result, d_ws, ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int vlz_minmax(const float* d_in, int64_t n, double* d_minmax, void* stream) {
+  if (!d_in || n < 1 || !d_minmax) return VLZ_E_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // 4 scratch words live in a lazily allocated device buffer per device
+  static unsigned int* scratch[64] = {nullptr};
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!scratch[dev]) {
+      cudaError_t e = cudaMalloc(&scratch[dev], 64);
+      if (e != cudaSuccess) return to_rc(e);
+    }
+  }
+  unsigned int* w = scratch[dev];
+  minmax_init<<<1, 1, 0, st>>>(w);
+  int64_t blocks = (n + 1023) / 1024;
+  const int64_t cap = (int64_t)num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  minmax_kernel<<<(unsigned)blocks, 256, 0, st>>>(d_in, n, w, w + 1, w + 2, w + 3, d_minmax);
+  g_launches.fetch_add(2, std::memory_order_relaxed);
+  return to_rc(cudaGetLastError());
+}
+
+// ---- host-buffer entry points ------------------------------------------
+namespace {
+struct HostCache {
+  int dev = -1;
+  cudaStream_t st = nullptr;
+  void* buf = nullptr;
+  size_t cap = 0;
+};
+HostCache g_host[64];
+std::mutex g_host_mu;
+
+void* host_buffer(int dev, size_t need, cudaStream_t& st) {
+  HostCache& c = g_host[dev];
+  if (!c.st) cudaStreamCreateWithFlags(&c.st, cudaStreamNonBlocking);
+  if (c.cap < need) {
+    if (c.buf) cudaFree(c.buf);
+    c.buf = nullptr;
+    c.cap = 0;
+    if (cudaMalloc(&c.buf, need) != cudaSuccess) return nullptr;
+    c.cap = need;
+  }
+  st = c.st;
+  return c.buf;
+}
+}  // namespace
+
+int vlz_dq_compress_host(const float* h_in, const vlz_geom* gg, const vlz_params* p,
+                         uint16_t* h_codes, float* h_outliers, int64_t* h_counts,
+                         int64_t* h_scalars, vlz_result* h_result, int device) {
+  Geo g;
+  if (!make_geo(gg, g) || !valid_params(p) || device < 0 || device >= 64) return VLZ_E_ARG;
+  std::lock_guard<std::mutex> lk(g_host_mu);
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  const int64_t ns = vlz_scalar_count(gg, p->pad_kind, p->pad_gran);
+  const size_t ws = vlz_workspace_size(gg);
+  const size_t o_in = 0, o_codes = align256(g.N * 4), o_out = o_codes + align256(g.N * 2),
+               o_cnt = o_out + align256(g.N * 4), o_sc = o_cnt + align256(g.nblocks * 8),
+               o_res = o_sc + align256((ns > 0 ? ns : 1) * 8), o_ws = o_res + 256,
+               total = o_ws + ws;
+  cudaStream_t st;
+  char* base = static_cast<char*>(host_buffer(device, total, st));
+  if (!base) {
+    cudaSetDevice(prev);
+    return VLZ_E_CUDA;
+  }
+  float* d_in = reinterpret_cast<float*>(base + o_in);
+  uint16_t* d_codes = reinterpret_cast<uint16_t*>(base + o_codes);
+  float* d_out = reinterpret_cast<float*>(base + o_out);
+  int64_t* d_cnt = reinterpret_cast<int64_t*>(base + o_cnt);
+  int64_t* d_sc = reinterpret_cast<int64_t*>(base + o_sc);
+  vlz_result* d_res = reinterpret_cast<vlz_result*>(base + o_res);
+  cudaMemcpyAsync(d_in, h_in, g.N * 4, cudaMemcpyHostToDevice, st);
+  int rc = vlz_dq_compress(d_in, gg, p, d_codes, d_out, d_cnt, d_sc, d_res, base + o_ws, ws, st);
+  if (rc == VLZ_OK) {
+    cudaMemcpyAsync(h_result, d_res, sizeof(vlz_result), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(h_codes, d_codes, g.N * 2, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(h_counts, d_cnt, g.nblocks * 8, cudaMemcpyDeviceToHost, st);
+    if (ns > 0) cudaMemcpyAsync(h_scalars, d_sc, ns * 8, cudaMemcpyDeviceToHost, st);
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess && h_result->status == VLZ_ST_OK && h_result->n_outliers > 0) {
+      cudaMemcpyAsync(h_outliers, d_out, h_result->n_outliers * 4, cudaMemcpyDeviceToHost, st);
+      e = cudaStreamSynchronize(st);
+    }
+    rc = to_rc(e);
+  }
+  cudaSetDevice(prev);
+  return rc;
+}
+
+int vlz_dq_decompress_host(const uint16_t* h_codes, const float* h_outliers, int64_t n_outliers,
+                           const int64_t* h_counts, const int64_t* h_scalars, const vlz_geom* gg,
+                           const vlz_params* p, float* h_out, vlz_result* h_result, int device) {
+  Geo g;
+  if (!make_geo(gg, g) || !valid_params(p) || device < 0 || device >= 64 || n_outliers < 0)
+    return VLZ_E_ARG;
+  std::lock_guard<std::mutex> lk(g_host_mu);
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  const int64_t ns = vlz_scalar_count(gg, p->pad_kind, p->pad_gran);
+  const size_t ws = vlz_workspace_size(gg);
+  const size_t o_codes = 0, o_ol = align256(g.N * 2), o_cnt = o_ol + align256(n_outliers * 4 + 4),
+               o_sc = o_cnt + align256(g.nblocks * 8),
+               o_out = o_sc + align256((ns > 0 ? ns : 1) * 8), o_res = o_out + align256(g.N * 4),
+               o_ws = o_res + 256, total = o_ws + ws;
+  cudaStream_t st;
+  char* base = static_cast<char*>(host_buffer(device, total, st));
+  if (!base) {
+    cudaSetDevice(prev);
+    return VLZ_E_CUDA;
+  }
+  uint16_t* d_codes = reinterpret_cast<uint16_t*>(base + o_codes);
+  float* d_ol = reinterpret_cast<float*>(base + o_ol);
+  int64_t* d_cnt = reinterpret_cast<int64_t*>(base + o_cnt);
+  int64_t* d_sc = reinterpret_cast<int64_t*>(base + o_sc);
+  float* d_out = reinterpret_cast<float*>(base + o_out);
+  vlz_result* d_res = reinterpret_cast<vlz_result*>(base + o_res);
+  cudaMemcpyAsync(d_codes, h_codes, g.N * 2, cudaMemcpyHostToDevice, st);
+  if (n_outliers > 0) cudaMemcpyAsync(d_ol, h_outliers, n_outliers * 4, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(d_cnt, h_counts, g.nblocks * 8, cudaMemcpyHostToDevice, st);
+  if (ns > 0) cudaMemcpyAsync(d_sc, h_scalars, ns * 8, cudaMemcpyHostToDevice, st);
+  int rc = vlz_dq_decompress(d_codes, d_ol, n_outliers, d_cnt, d_sc, gg, p, d_out, d_res,
+                             base + o_ws, ws, st);
+  if (rc == VLZ_OK) {
+    cudaMemcpyAsync(h_result, d_res, sizeof(vlz_result), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(h_out, d_out, g.N * 4, cudaMemcpyDeviceToHost, st);
+    rc = to_rc(cudaStreamSynchronize(st));
+  }
+  cudaSetDevice(prev);
+  return rc;
+}
+
+void vlz_host_release(void) {
+  std::lock_guard<std::mutex> lk(g_host_mu);
+  for (auto& c : g_host) {
+    if (c.buf) cudaFree(c.buf);
+    c.buf = nullptr;
+    c.cap = 0;
+  }
+}
+
+int64_t vlz_launch_count(void) { return g_launches.load(); }
+
+const char* vlz_version(void) { return "vlz_gpu 0.1 sm_100a"; }
+
+}  // extern "C"

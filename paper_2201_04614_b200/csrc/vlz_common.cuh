@@ -1,0 +1,147 @@
+// vlz_common.cuh -- geometry, exact quantizer arithmetic and warp helpers
+// shared by the dual-quant kernels (sm_100a).
+//
+// Reference semantics restated here (paths relative to
+// /root/reference/pkg/src/vlz/):
+//   quantize.py:31-42,50-79   prequantization q = fl64(v / (2 eb)),
+//                             d = sign(q) * floor(|q| + 0.5), overflow at 2^31-1
+//   quantize.py:45-47,82-84   reconstruction float32((2.0 * d) * eb)
+//   vector.py:72-78           outlier iff |delta| > R-1 or the float32-narrowed
+//                             reconstruction misses the bound
+//   padding.py:53-59          exact half-away rounding of an int64 mean
+//   model.py:113-159          row-major block grid, partial edge blocks
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace vlz {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+// Padded 3-D view of a 1/2/3-D array: dims (D0, D1, D2) with leading 1s, so a
+// 1-D array is (1, 1, N) and a 2-D array (1, Y, X).  Block extents per padded
+// dim are (BZ, BY, BX) = (B if nd == 3 else 1, B if nd >= 2 else 1, B).
+struct Geo {
+  int64_t D0, D1, D2;
+  int64_t P0, P1, P2;  // blocks per padded dim
+  int64_t NW;          // windows of W columns per block row
+  int64_t ntiles;      // P0 * P1 * NW
+  int64_t nblocks;
+  int64_t N;
+};
+
+struct QP {
+  double eb;     // resolved absolute bound
+  double twoeb;  // 2.0 * eb (exact)
+  int radius;
+  int kind;      // VLZ_PAD_* (min / max / mean used by the statistics)
+};
+
+// canonical start of a block's codes: number of in-bounds elements of all
+// earlier blocks in row-major block order (vector.py:193-202 ordering)
+__host__ __device__ __forceinline__ int64_t block_start(const Geo& g, int64_t bz, int64_t by,
+                                                        int64_t bx, int BZ, int BY, int BX,
+                                                        int64_t ez, int64_t ey) {
+  const int64_t o0 = bz * BZ, o1 = by * BY, o2 = bx * BX;
+  return o0 * g.D1 * g.D2 + ez * o1 * g.D2 + ez * ey * o2;
+}
+
+__device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+__device__ __forceinline__ int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }
+
+// quantize.py:31-42 + vector.py:72-78, exact IEEE float64 evaluation.
+//   n    = round_half_away(fl64(v / (2 eb)))
+//   bad  = |f64(f32(fl64((2.0 * n) * eb))) - f64(v)| > eb   (narrowing check)
+//   ovf  = !(|q| < 2^31 - 1)     (also true for NaN)
+__device__ __forceinline__ int quant_exact(float v, const QP& q, bool& bad, bool& ovf) {
+  const double dv = (double)v;
+  const double qq = __ddiv_rn(dv, q.twoeb);
+  const double a = fabs(qq);
+  ovf = !(a < 2147483647.0);
+  const double fl = floor(__dadd_rn(a, 0.5));
+  const int m = ovf ? 0 : (int)fl;
+  const int n = (qq < 0.0) ? -m : m;
+  const float w = __double2float_rn(__dmul_rn(2.0 * (double)n, q.eb));
+  bad = fabs(__dsub_rn((double)w, dv)) > q.eb;
+  return n;
+}
+
+// quantize.py:40-42 for reconstruction of sentinel values (no overflow
+// guard in the reference's decompressor; values of valid streams fit).
+__device__ __forceinline__ int64_t quant_value(float v, double twoeb) {
+  const double qq = __ddiv_rn((double)v, twoeb);
+  const double a = fabs(qq);
+  const double fl = floor(__dadd_rn(a, 0.5));
+  const long long m = (a < 9.2e18) ? (long long)fl : 0;
+  return qq < 0.0 ? -m : m;
+}
+
+// quantize.py:45-47: float32((2.0 * d) * eb)
+__device__ __forceinline__ float dequant(int64_t d, double eb) {
+  return __double2float_rn(__dmul_rn(2.0 * (double)d, eb));
+}
+
+// padding.py:53-59 (total is the int64 wrapping sum)
+__host__ __device__ __forceinline__ int64_t round_half_away_ratio(int64_t total, int64_t count) {
+  if (count <= 0) return 0;
+  const uint64_t mag = total < 0 ? 0ull - (uint64_t)total : (uint64_t)total;
+  const uint64_t qq = mag / (uint64_t)count, r = mag % (uint64_t)count;
+  const uint64_t res = qq + ((2 * r >= (uint64_t)count) ? 1 : 0);
+  return total < 0 ? -(int64_t)res : (int64_t)res;
+}
+
+// padding.py:62-69
+__host__ __device__ __forceinline__ int64_t stat_value(int kind, int64_t sum, int64_t cnt,
+                                                       int64_t mn, int64_t mx) {
+  if (kind == 1) return mn;  // VLZ_PAD_MIN
+  if (kind == 2) return mx;  // VLZ_PAD_MAX
+  return round_half_away_ratio(sum, cnt);
+}
+
+// ---- segmented warp helpers over aligned groups of L lanes ------------
+template <int L, typename T>
+__device__ __forceinline__ T group_sum(T v) {
+#pragma unroll
+  for (int o = L / 2; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+template <int L, typename T>
+__device__ __forceinline__ T group_min(T v) {
+#pragma unroll
+  for (int o = L / 2; o > 0; o >>= 1) {
+    T u = __shfl_xor_sync(FULL, v, o);
+    v = u < v ? u : v;
+  }
+  return v;
+}
+template <int L, typename T>
+__device__ __forceinline__ T group_max(T v) {
+#pragma unroll
+  for (int o = L / 2; o > 0; o >>= 1) {
+    T u = __shfl_xor_sync(FULL, v, o);
+    v = u > v ? u : v;
+  }
+  return v;
+}
+template <int L>
+__device__ __forceinline__ bool group_any(bool b, int lane) {
+  const unsigned m = __ballot_sync(FULL, b);
+  const unsigned gm = (L == 32) ? FULL : (((1u << L) - 1u) << (lane & ~(L - 1)));
+  return (m & gm) != 0;
+}
+// exclusive prefix sum within the group (int)
+template <int L>
+__device__ __forceinline__ int group_excl_scan(int v, int lane, int& total) {
+  int inc = v;
+  const int gl = lane & (L - 1);
+#pragma unroll
+  for (int o = 1; o < L; o <<= 1) {
+    int u = __shfl_up_sync(FULL, inc, o);
+    if (gl >= o) inc += u;
+  }
+  total = __shfl_sync(FULL, inc, (lane & ~(L - 1)) + L - 1);
+  return inc - v;
+}
+
+}  // namespace vlz

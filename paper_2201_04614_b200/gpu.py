@@ -1,0 +1,251 @@
+"""Device-level API: run the dual-quant kernels on CUDA tensors.
+
+PyTorch is only the tensor/stream plumbing here: every computation happens
+in libvlzgpu.so (paper_2201_04614_b200/csrc).  Results stay on the device;
+`check()` reads back the 64-byte status block and raises the reference's
+exception for it (errors.py; reference quantize.py:58-72, reconstruct.py:
+43-66,87-91).
+
+    dev = compress_device(x, config)            # x: cuda float32 tensor
+    dev.check()                                  # raises on bad input
+    y = decompress_device(dev)                   # cuda float32 tensor
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import BoundTooSmallError, ConfigError, CorruptStreamError
+from .model import (
+    ArrayDescriptor,
+    BlockGrid,
+    CompressionConfig,
+    ErrorBound,
+    ErrorBoundMode,
+    PaddingPolicy,
+    PaddingValue,
+    build_block_grid,
+    resolve_error_bound_from_range,
+)
+
+
+def _ptr(t) -> int:
+    return 0 if t is None else t.data_ptr()
+
+
+def _stream(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def value_range(x: torch.Tensor, stream=None):
+    """(float(min), float(max)) of a float32 CUDA tensor, NaN-propagating like
+    numpy (model.py:104-107).  Synchronises."""
+    lib = _lib.load()
+    out = torch.empty(2, dtype=torch.float64, device=x.device)
+    rc = lib.vlz_minmax(_ptr(x), x.numel(), _ptr(out), _stream(stream))
+    if rc != 0:
+        raise RuntimeError(f"vlz_minmax failed ({rc})")
+    lo, hi = out.tolist()
+    return lo, hi
+
+
+def resolve_eb_device(eb: ErrorBound, x: torch.Tensor) -> float:
+    if x.numel() == 0:
+        raise ConfigError("cannot resolve an error bound for empty data")
+    if eb.mode is ErrorBoundMode.ABSOLUTE:
+        return float(eb.value)
+    lo, hi = value_range(x)
+    return resolve_error_bound_from_range(eb, lo, hi)
+
+
+@dataclass
+class DeviceCodeStream:
+    """CodeStream fields as CUDA tensors (codes uint16 as int16 storage)."""
+
+    codes: torch.Tensor            # int16 [N], reinterpret as uint16
+    outliers: torch.Tensor         # float32 [N] capacity, first n_outliers valid
+    counts: torch.Tensor           # int64 [nblocks]
+    scalars: torch.Tensor          # int64 [scalar_count]
+    result: torch.Tensor           # int64 [8] = vlz_result
+    grid: BlockGrid
+    eb: float
+    radius: int
+    padding: PaddingPolicy
+    source: torch.Tensor = None    # input (kept for error reporting)
+    _host_result: object = None
+
+    @property
+    def shape(self):
+        return self.grid.descriptor.dims
+
+    def read_result(self) -> _lib.Result:
+        if self._host_result is None:
+            r = _lib.Result()
+            buf = self.result.cpu().numpy()
+            ctypes.memmove(ctypes.byref(r), buf.ctypes.data, 64)
+            self._host_result = r
+        return self._host_result
+
+    @property
+    def n_outliers(self) -> int:
+        return int(self.read_result().n_outliers)
+
+    def check(self) -> "DeviceCodeStream":
+        r = self.read_result()
+        if r.status == _lib.ST_NONFINITE:
+            raise ConfigError(f"data contains a non-finite value at flat index {r.index}")
+        if r.status == _lib.ST_OVERFLOW:
+            v = float(self.source.reshape(-1)[r.index].item()) if self.source is not None else float("nan")
+            raise BoundTooSmallError(int(r.index), v, self.eb)
+        if r.status != _lib.ST_OK:
+            raise RuntimeError(f"unexpected compress status {r.status}")
+        return self
+
+    def outlier_values(self) -> torch.Tensor:
+        return self.outliers[: self.n_outliers]
+
+
+def _alloc_like(n, dtype, device):
+    return torch.empty(max(int(n), 1), dtype=dtype, device=device)
+
+
+class Workspace:
+    """Grow-only device workspace cache (one per device)."""
+
+    _cache = {}
+
+    @classmethod
+    def get(cls, nbytes: int, device) -> torch.Tensor:
+        key = (device.type, device.index)
+        ws = cls._cache.get(key)
+        if ws is None or ws.numel() < nbytes:
+            ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+            cls._cache[key] = ws
+        return ws
+
+
+def compress_device(x: torch.Tensor, config: CompressionConfig, eb: float = None,
+                    stream=None, workspace: torch.Tensor = None,
+                    out: DeviceCodeStream = None) -> DeviceCodeStream:
+    """Fused dual-quant compress of a CUDA float32 tensor (no host sync unless
+    the bound is value-range relative)."""
+    if not x.is_cuda:
+        raise ConfigError("compress_device needs a CUDA tensor")
+    desc = ArrayDescriptor.from_array(x)
+    grid = build_block_grid(desc, config.block_edge)
+    if desc.ndims != 1 and config.block_edge == 256:
+        raise ConfigError("block edge 256 is supported for 1-D arrays only")
+    if eb is None:
+        eb = resolve_eb_device(config.error_bound, x)
+    if eb <= 0.0:
+        raise ConfigError(f"resolved error bound must be > 0, got {eb}")
+    x = x.contiguous()
+    lib = _lib.load()
+    g = _lib.geom(desc.dims, config.block_edge)
+    pol = config.padding
+    p = _lib.params(eb, config.radius, pol.kind_code, pol.gran_code)
+    n = desc.element_count
+    ns = pol.scalar_count(grid)
+    dev = x.device
+    if out is None:
+        out = DeviceCodeStream(
+            codes=_alloc_like(n, torch.int16, dev),
+            outliers=_alloc_like(n, torch.float32, dev),
+            counts=_alloc_like(grid.block_count, torch.int64, dev),
+            scalars=torch.empty(ns, dtype=torch.int64, device=dev),
+            result=torch.empty(8, dtype=torch.int64, device=dev),
+            grid=grid, eb=eb, radius=config.radius, padding=pol, source=x,
+        )
+    else:
+        out.grid, out.eb, out.radius, out.padding, out.source = grid, eb, config.radius, pol, x
+        out._host_result = None
+    wsb = lib.vlz_workspace_size(ctypes.byref(g))
+    ws = workspace if workspace is not None else Workspace.get(wsb, dev)
+    rc = lib.vlz_dq_compress(
+        _ptr(x), ctypes.byref(g), ctypes.byref(p), _ptr(out.codes), _ptr(out.outliers),
+        _ptr(out.counts), _ptr(out.scalars) if ns else None, _ptr(out.result), _ptr(ws),
+        ws.numel(), _stream(stream),
+    )
+    if rc != 0:
+        raise RuntimeError(f"vlz_dq_compress failed ({rc})")
+    return out
+
+
+def block_span(grid: BlockGrid, bi: int):
+    """(start, size) of block bi in the canonical code stream."""
+    dims = grid.descriptor.dims
+    nd = len(dims)
+    org = grid.block_origin(bi)
+    ext = grid.block_extents(bi)
+    if nd == 1:
+        start = org[0]
+    elif nd == 2:
+        start = org[0] * dims[1] + ext[0] * org[1]
+    else:
+        start = org[0] * dims[1] * dims[2] + ext[0] * org[1] * dims[2] + ext[0] * ext[1] * org[2]
+    return start, int(np.prod(ext))
+
+
+def decompress_device(codes: torch.Tensor, outliers: torch.Tensor, n_outliers: int,
+                      counts: torch.Tensor, scalars: torch.Tensor, grid: BlockGrid, eb: float,
+                      radius: int, padding: PaddingPolicy, out: torch.Tensor = None,
+                      result: torch.Tensor = None, stream=None, workspace=None,
+                      check: bool = True) -> torch.Tensor:
+    """Fused reconstruction (reconstruct.py:74-124 minus Huffman decode).
+    codes: int16 (uint16 storage) or int32 (uint32 storage) CUDA tensor."""
+    lib = _lib.load()
+    desc = grid.descriptor
+    g = _lib.geom(desc.dims, grid.block_edge)
+    p = _lib.params(eb, radius, padding.kind_code, padding.gran_code)
+    dev = codes.device
+    if out is None:
+        out = torch.empty(desc.dims, dtype=torch.float32, device=dev)
+    if result is None:
+        result = torch.empty(8, dtype=torch.int64, device=dev)
+    wsb = lib.vlz_workspace_size(ctypes.byref(g))
+    ws = workspace if workspace is not None else Workspace.get(wsb, dev)
+    fn = lib.vlz_dq_decompress if codes.element_size() == 2 else lib.vlz_dq_decompress_u32
+    rc = fn(_ptr(codes), _ptr(outliers) if n_outliers else None, int(n_outliers), _ptr(counts),
+            _ptr(scalars) if scalars is not None and scalars.numel() else None, ctypes.byref(g),
+            ctypes.byref(p), _ptr(out), _ptr(result), _ptr(ws), ws.numel(), _stream(stream))
+    if rc != 0:
+        raise RuntimeError(f"vlz_dq_decompress failed ({rc})")
+    if check:
+        check_decompress(result, codes, counts, n_outliers, grid, radius)
+    return out
+
+
+def check_decompress(result: torch.Tensor, codes, counts, n_outliers, grid, radius):
+    r = _lib.Result()
+    buf = result.cpu().numpy()
+    ctypes.memmove(ctypes.byref(r), buf.ctypes.data, 64)
+    if r.status == _lib.ST_OK:
+        return
+    if r.status == _lib.ST_SENTINEL_TOTAL:
+        raise CorruptStreamError(f"{r.n_outliers} sentinel codes but {n_outliers} outliers")
+    bi = int(r.index)
+    start, size = block_span(grid, bi)
+    blk = codes[start:start + size].cpu().numpy()
+    blk = blk.view(np.uint16) if blk.dtype == np.int16 else blk.view(np.uint32)
+    if r.status == _lib.ST_CORRUPT_CODE:
+        raise CorruptStreamError(f"code {int(blk.max())} out of range for radius {radius}")
+    if r.status == _lib.ST_EXHAUSTED:
+        raise CorruptStreamError("outlier list exhausted before sentinels")
+    if r.status == _lib.ST_LEFTOVER:
+        cnt = counts.cpu().numpy()
+        off = int(cnt[:bi].sum())
+        avail = max(0, min(int(cnt[bi]), int(n_outliers) - off))
+        raise CorruptStreamError(
+            f"block consumed {int((blk == 0).sum())} outliers but {avail} were stored"
+        )
+    raise RuntimeError(f"unexpected decompress status {r.status}")
+
+
+def launch_count() -> int:
+    return int(_lib.load().vlz_launch_count())

@@ -1,0 +1,41 @@
+"""GPU drop-in for the reference decompressor's block loop.
+
+reference reconstruct.py:74-124 (decompress_parsed) decodes the Huffman
+stream and then runs reconstruct_block (reconstruct.py:30-71) per block.
+`reconstruct_stream` is that block loop on the GPU: it takes the decoded
+code stream (CodeStream fields) and returns the float32 array, byte-identical
+to the reference, raising the same CorruptStreamError messages for
+inconsistent streams.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import gpu
+from .model import BlockGrid, CodeStream, PaddingPolicy
+
+
+def reconstruct_arrays(codes: np.ndarray, outlier_values: np.ndarray, outlier_counts: np.ndarray,
+                       scalars: np.ndarray, grid: BlockGrid, eb: float, radius: int,
+                       padding: PaddingPolicy) -> np.ndarray:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2201_04614_b200 needs a CUDA device (B200); no CPU fallback")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    codes = np.ascontiguousarray(codes)
+    if codes.dtype == np.uint16:
+        c = torch.from_numpy(codes.view(np.int16)).to(dev)
+    else:
+        c = torch.from_numpy(codes.astype(np.uint32, copy=False).view(np.int32)).to(dev)
+    ov = torch.from_numpy(np.ascontiguousarray(outlier_values, dtype=np.float32)).to(dev)
+    cnt = torch.from_numpy(np.ascontiguousarray(outlier_counts, dtype=np.int64)).to(dev)
+    sc = torch.from_numpy(np.ascontiguousarray(scalars, dtype=np.int64)).to(dev)
+    out = gpu.decompress_device(c, ov, ov.numel(), cnt, sc, grid, eb, radius, padding)
+    return out.cpu().numpy()
+
+
+def reconstruct_stream(stream: CodeStream) -> np.ndarray:
+    return reconstruct_arrays(stream.codes, stream.outlier_values, stream.outlier_counts,
+                              stream.scalars.values, stream.grid, stream.resolved_abs,
+                              stream.radius, stream.scalars.policy)

@@ -1,0 +1,227 @@
+"""Parity of the CUDA path (libvlzgpu.so) with the reference.
+
+* golden corpus: byte equality with streams and decompressed arrays produced
+  by the reference itself (tests/golden/make_golden.py);
+* full size (BASELINE.json C1-C4): equality with the reference's sha256 (C1,
+  C2) or with the pinned CPU oracle (C3, C4, outlier stress), plus the
+  size-independent properties: error bound, exact round trip, idempotent
+  recompression.
+All calls go through the C ABI (ctypes), no CPU fallback exists."""
+
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import load_json
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2201_04614_b200 import gpu, workloads  # noqa: E402
+from paper_2201_04614_b200 import model as M  # noqa: E402
+from paper_2201_04614_b200.errors import (  # noqa: E402
+    BoundTooSmallError,
+    ConfigError,
+    CorruptStreamError,
+    DegenerateRangeError,
+)
+from paper_2201_04614_b200.reconstruct import reconstruct_arrays, reconstruct_stream  # noqa: E402
+from paper_2201_04614_b200.vector import dualquant, dualquant_vector  # noqa: E402
+
+M.allow_block_256(True)
+
+
+def _cfg(eb, b, pol, radius, lanes=8):
+    return M.CompressionConfig(M.ErrorBound.absolute(eb), block_edge=b, lane_width=lanes,
+                               padding=M.PaddingPolicy.parse(pol), radius=radius)
+
+
+def _sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def test_corpus_compress_matches_reference(corpus_cases):
+    for c in corpus_cases:
+        s = dualquant_vector(c["data"], _cfg(c["eb"], c["block_edge"], c["padding"], c["radius"]))
+        tag = c["tag"]
+        assert s.codes.dtype == np.uint32
+        assert np.array_equal(s.codes, c["codes"].astype(np.uint32)), tag
+        assert s.outlier_values.tobytes() == c["outlier_values"].tobytes(), tag
+        assert np.array_equal(s.outlier_counts, c["outlier_counts"]), tag
+        assert np.array_equal(s.scalars.values, c["scalars"]), tag
+
+
+def test_corpus_decompress_matches_reference(corpus_cases):
+    n = 0
+    for c in corpus_cases:
+        if "decompressed" not in c:
+            continue
+        grid = M.build_block_grid(M.ArrayDescriptor(len(c["shape"]), tuple(c["shape"])),
+                                  c["block_edge"])
+        for codes in (c["codes"], c["codes"].astype(np.uint32)):  # u16 and u32 kernels
+            out = reconstruct_arrays(codes, c["outlier_values"], c["outlier_counts"],
+                                     c["scalars"], grid, c["eb"], c["radius"],
+                                     M.PaddingPolicy.parse(c["padding"]))
+            assert out.tobytes() == c["decompressed"].tobytes(), c["tag"]
+        n += 1
+    assert n > 50
+
+
+def test_corpus_round_trip_matches_oracle(oracle, corpus_cases):
+    for c in corpus_cases:
+        grid = M.build_block_grid(M.ArrayDescriptor(len(c["shape"]), tuple(c["shape"])),
+                                  c["block_edge"])
+        out = reconstruct_arrays(c["codes"], c["outlier_values"], c["outlier_counts"],
+                                 c["scalars"], grid, c["eb"], c["radius"],
+                                 M.PaddingPolicy.parse(c["padding"]))
+        ref = oracle.reconstruct(c["codes"].astype(np.uint32), c["outlier_values"],
+                                 c["outlier_counts"], c["scalars"], tuple(c["shape"]),
+                                 c["block_edge"], c["eb"], c["radius"], c["padding"])
+        assert out.tobytes() == ref.tobytes(), c["tag"]
+        err = np.abs(out.astype(np.float64) - c["data"].astype(np.float64))
+        assert err.max(initial=0.0) <= c["eb"], c["tag"]
+
+
+def test_error_cases():
+    for c in load_json("errors.json"):
+        data = np.array(c["data"], dtype=np.float32).reshape(c["shape"])
+        exp = c["expect"]
+        if c["eb"] is None:
+            cfg = M.CompressionConfig(M.ErrorBound.relative(c["rel"]), block_edge=c["block_edge"])
+        else:
+            cfg = _cfg(c["eb"], c["block_edge"], c["padding"], 32768)
+        if exp is None:
+            dualquant_vector(data, cfg)
+            continue
+        cls = {"ConfigError": ConfigError, "BoundTooSmallError": BoundTooSmallError,
+               "DegenerateRangeError": DegenerateRangeError}[exp["type"]]
+        with pytest.raises(cls) as err:
+            dualquant_vector(data, cfg)
+        assert str(err.value) == exp["message"], c["tag"]
+        assert type(err.value) is cls
+
+
+def test_corrupt_streams(corrupt_cases):
+    for c in corrupt_cases:
+        grid = M.build_block_grid(M.ArrayDescriptor(len(c["shape"]), tuple(c["shape"])),
+                                  c["block_edge"])
+        with pytest.raises(CorruptStreamError) as err:
+            reconstruct_arrays(c["codes"], c["outlier_values"], c["outlier_counts"], c["scalars"],
+                               grid, c["eb"], c["radius"], M.PaddingPolicy.parse(c["padding"]))
+        assert str(err.value) == c["expect"]["message"], c["tag"]
+
+
+def test_lane_width_rules():
+    data = np.zeros(8, dtype=np.float32)
+    with pytest.raises(ConfigError):
+        dualquant_vector(data, M.CompressionConfig(M.ErrorBound.absolute(1e-4), lane_width=1))
+    d = np.random.default_rng(0).uniform(-10, 10, (20, 12)).astype(np.float32)
+    ref = dualquant(d, _cfg(1e-4, 8, "mean:global", 32768, lanes=1))
+    for lanes in (4, 8, 16):
+        assert dualquant_vector(d, _cfg(1e-4, 8, "mean:global", 32768, lanes)).same_bytes(ref)
+
+
+def test_border_stats_constant_field():
+    data = np.full((16, 16), 100.0, dtype=np.float32)
+    _, (total, border) = dualquant_vector(data, _cfg(1e-4, 8, "zero", 32768), collect_border=True)
+    assert total == 4 and border == 4
+
+
+# ---------------------------------------------------------------- full size
+
+
+def _check_full(oracle, data, eb, b, pol, radius, ref_hashes=None):
+    cfg = _cfg(eb, b, pol, radius)
+    s = dualquant(data, cfg)
+    if ref_hashes is not None:
+        assert _sha(s.codes.astype(np.uint16)) == ref_hashes["codes_u16_sha"]
+        assert _sha(s.outlier_values) == ref_hashes["outliers_sha"]
+        assert _sha(s.outlier_counts) == ref_hashes["counts_sha"]
+        assert _sha(s.scalars.values) == ref_hashes["scalars_sha"]
+    else:
+        o = oracle.dualquant(data, eb, b, radius, pol)
+        assert np.array_equal(s.codes, o["codes"])
+        assert s.outlier_values.tobytes() == o["outlier_values"].tobytes()
+        assert np.array_equal(s.outlier_counts, o["outlier_counts"])
+        assert np.array_equal(s.scalars.values, o["scalars"])
+    back = reconstruct_stream(s)
+    # size-independent properties: bound, exact inverse, idempotence
+    err = np.abs(back.astype(np.float64) - data.astype(np.float64))
+    assert err.max() <= eb
+    # closed form of the exact inverse (DESIGN.md finding 2): verbatim value
+    # at outliers, float32((2 d) eb) with d the prequantized value elsewhere
+    qd = oracle.prequantize(data, eb)
+    recon = ((2.0 * qd.astype(np.float64)) * eb).astype(np.float32).ravel()
+    mask = _outlier_mask_rowmajor(s, data.shape)
+    assert int(mask.sum()) == s.outlier_values.size
+    expected = np.where(mask, data.ravel(), recon)
+    assert back.ravel().tobytes() == expected.tobytes()
+    again = dualquant(back, cfg)
+    assert again.same_bytes(s)
+    return s
+
+
+def _outlier_mask_rowmajor(s, shape):
+    """Row-major mask of outlier positions from the canonical code stream."""
+    grid = s.grid
+    m = np.zeros(shape, dtype=bool)
+    nd = len(shape)
+    pos = 0
+    codes = s.codes
+    # walk blocks; vectorised per block
+    for bi in range(grid.block_count):
+        org = grid.block_origin(bi)
+        ext = grid.block_extents(bi)
+        size = int(np.prod(ext))
+        if s.outlier_counts[bi]:
+            blk = codes[pos:pos + size].reshape(ext) == 0
+            m[tuple(slice(o, o + e) for o, e in zip(org, ext))] = blk
+        pos += size
+    assert nd in (1, 2, 3)
+    return m.ravel()
+
+
+def test_fullsize_c1_c2_match_reference_hashes(oracle):
+    data = {"C1": workloads.gen_c1(), "C2": workloads.gen_c2()}
+    for c in load_json("fullsize.json"):
+        d = data[c["config"]]
+        same_data = _sha(d) == c["data_sha"]
+        _check_full(oracle, d, c["eb"], c["block_edge"], c["padding"], c["radius"],
+                    ref_hashes=c if same_data else None)
+
+
+def test_fullsize_c3_matches_oracle(oracle):
+    d = workloads.gen_c3()
+    eb = workloads.value_range_eb(d, 1e-3)
+    _check_full(oracle, d, eb, 8, "mean:global", 512)
+    _check_full(oracle, d, eb, 8, "mean:block", 512)
+
+
+def test_fullsize_c4_matches_oracle(oracle):
+    d = workloads.gen_c4(512)
+    eb = workloads.value_range_eb(d, 1e-3)
+    for b, r in ((8, 512), (16, 32768)):
+        _check_full(oracle, d, eb, b, "mean:global", r)
+
+
+def test_outlier_stress_matches_oracle(oracle):
+    # C4 field at eb = 1e-5 * range: ~18% outliers at R=512
+    d = workloads.gen_c4(128)
+    eb = workloads.value_range_eb(d, 1e-5)
+    for pol in ("zero", "max:edge", "min:block"):
+        s = _check_full(oracle, d, eb, 8, pol, 512)
+        assert s.outlier_values.size > 0.05 * d.size
+
+
+def test_int64_redo_path(oracle):
+    # |d| >= 2^28 forces the int64 stencil redo (dq_compress.cuh)
+    rng = np.random.default_rng(3)
+    d = (rng.uniform(-1, 1, (40, 33, 70)) * 1.0e9).astype(np.float32)
+    for pol in ("mean:global", "zero", "max:block", "min:edge"):
+        _check_full(oracle, d, 0.9, 8, pol, 32768)
