@@ -1,0 +1,466 @@
+#!/usr/bin/env python
+"""Benchmark of the dual-quant hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json config 5): a 2048x2048x1024 float32 field (16 GiB),
+64 random 3-D sinusoidal modes + N(0,1e-3) noise generated on the device,
+block 8x8x8, eb = 1e-4 * value range, radius 512, mean:global padding,
+z-slab-sharded (block aligned, no halo) over N GPUs -- strong scaling of the
+fixed 16 GiB field.  One step = compress + decompress of the whole field:
+  compress   = fused prequant/Lorenzo/postquant kernel, NCCL all-reduce of the
+               global padding statistics (N>1), origin fix + outlier compaction,
+               NCCL all-gather of per-shard outlier totals (N>1);
+  decompress = offsets scan + fused prefix-sum reconstruction.
+value = aggregate input GB/s of the round trip (4 bytes x elements / step
+time, max over ranks).  Inputs (17.2 GB) exceed the 126 MB L2, so no flush is
+needed between steps.  Per-kernel CUDA-event times give the roofline line;
+`e2e` is the same metric through the C-ABI host-buffer entry points
+(vlz_dq_compress_host / vlz_dq_decompress_host, pinned buffers, H2D + D2H in
+the timed region) on a 2 GiB slab per rank; `cpu_baseline` / --impl reference
+is the CPU oracle (oracle/, the reference's algorithm restated in C, OpenMP
+over all host cores) on a bounded slab of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "dual-quant compress/decompress GB/s per B200 and % HBM roofline at 1/2/4/8 GPU"
+SHAPE = (2048, 2048, 1024)
+BLOCK, RADIUS, PADDING, REL_EB = 8, 512, "mean:global", 1e-4
+FALLBACK_HBM = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--planes", type=int, default=SHAPE[0], help="dim-0 extent (debug)")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ helpers
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def hbm_peak():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.thread is not None:
+            self.thread.join(timeout=2)
+        rows = [r for r in self.rows if r[0].isdigit()]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [int(r[0]) for r in rows]
+        mx = max(int(r[1]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i] == "Active"})
+        return {"sm_mhz": int(statistics.median(sm)), "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ------------------------------------------------------------------ CPU arms
+
+
+def oracle_round_trip(sample: np.ndarray, eb: float, threads: int):
+    """One compress + decompress of `sample` by the CPU oracle; returns seconds."""
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import oracle
+
+    t0 = time.perf_counter()
+    s = oracle.dualquant(sample, eb, BLOCK, RADIUS, PADDING, threads=threads)
+    oracle.reconstruct(s["codes"], s["outlier_values"], s["outlier_counts"], s["scalars"],
+                       sample.shape, BLOCK, eb, RADIUS, PADDING, threads=threads)
+    return time.perf_counter() - t0
+
+
+CPU_PLANES = 8  # bounded CPU sample: 8 x 2048 x 1024 = 16.8M elements (67 MB)
+
+
+def run_reference(args):
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return  # the reference arm runs on rank 0 only
+    from paper_2201_04614_b200 import workloads
+
+    threads = os.cpu_count() or 1
+    sample = workloads.gen_c5_slab_numpy((0, CPU_PLANES))
+    eb = REL_EB * (float(sample.max()) - float(sample.min()))
+    for _ in range(args.warmup):
+        oracle_round_trip(sample, eb, threads)
+    times = [oracle_round_trip(sample, eb, threads) for _ in range(args.steps)]
+    tot = sum(times)
+    value = 4.0 * sample.size * args.steps / tot / 1e9
+    desc = (f"C5 slab {sample.shape[0]}x{SHAPE[1]}x{SHAPE[2]} ({sample.size} elements) "
+            f"compress+decompress round trip per step")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64+int64", "data": "synthetic (C5 recipe, numpy float64)",
+        "config": workload_config(args.gpus, eb),
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "port",
+                         "sample": desc},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(n, eb):
+    return {"workload": "C5: 2048x2048x1024 float32 3D (16 GiB), Lorenzo-3D block 8x8x8, "
+                        "eb=1e-4*range, radius 512, mean:global padding, compress+decompress",
+            "shape": list(SHAPE), "block_edge": BLOCK, "radius": RADIUS, "padding": PADDING,
+            "eb_rel": REL_EB, "eb": eb, "parallelism": f"z-slab x{n}",
+            "l2": "no flush: 17.2 GB input per step > 126 MB L2"}
+
+
+# ------------------------------------------------------------------ GPU arm
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2201_04614_b200 import _lib, gpu, workloads
+    from paper_2201_04614_b200 import model as M
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    lib = _lib.load()
+
+    D0 = args.planes
+    shape = (D0,) + SHAPE[1:]
+    assert D0 % (BLOCK * ws) == 0, "slabs must be block aligned"
+    per = D0 // ws
+    z0, z1 = rank * per, (rank + 1) * per
+    x = workloads.gen_c5_slab(z_range=(z0, z1), device=dev, shape=shape)
+    torch.cuda.synchronize()
+
+    # eb = 1e-4 * global value range (outside the timed region, like the reference)
+    mm = torch.empty(2, dtype=torch.float64, device=dev)
+    lib.vlz_minmax(x.data_ptr(), x.numel(), mm.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    if ws > 1:
+        lo = mm[0:1].clone()
+        hi = mm[1:2].clone()
+        dist.all_reduce(lo, op=dist.ReduceOp.MIN)
+        dist.all_reduce(hi, op=dist.ReduceOp.MAX)
+        mm = torch.cat([lo, hi])
+    lo, hi = mm.tolist()
+    eb = REL_EB * (hi - lo)
+
+    cfg = M.CompressionConfig(M.ErrorBound.absolute(eb), block_edge=BLOCK, radius=RADIUS,
+                              padding=M.PaddingPolicy.parse(PADDING))
+    pol = cfg.padding
+    desc = M.ArrayDescriptor(3, (per,) + SHAPE[1:])
+    grid = M.build_block_grid(desc, BLOCK)
+    g = _lib.geom(desc.dims, BLOCK)
+    p = _lib.params(eb, RADIUS, pol.kind_code, pol.gran_code)
+    n = desc.element_count
+    codes = torch.empty(n, dtype=torch.int16, device=dev)
+    outl = torch.empty(n, dtype=torch.float32, device=dev)
+    counts = torch.empty(grid.block_count, dtype=torch.int64, device=dev)
+    scalars = torch.empty(1, dtype=torch.int64, device=dev)
+    res = torch.empty(8, dtype=torch.int64, device=dev)
+    dres = torch.empty(8, dtype=torch.int64, device=dev)
+    stats = torch.empty(4, dtype=torch.int64, device=dev)
+    y = torch.empty_like(x)
+    wsb = lib.vlz_workspace_size(ctypes.byref(g))
+    wspace = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    totals = torch.empty(ws, dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    t_c = [0.0]
+    t_d = [0.0]
+
+    def step(timed):
+        if timed:
+            ev[0].record(stream)
+        rc = lib.vlz_dq_compress_begin(x.data_ptr(), ctypes.byref(g), ctypes.byref(p),
+                                       codes.data_ptr(), counts.data_ptr(), scalars.data_ptr(),
+                                       res.data_ptr(), stats.data_ptr(), wspace.data_ptr(), wsb, sp)
+        assert rc == 0
+        if ws > 1:
+            dist.all_reduce(stats[0:2], op=dist.ReduceOp.SUM)
+            dist.all_reduce(stats[2:4], op=dist.ReduceOp.MIN)
+        rc = lib.vlz_dq_compress_finish(x.data_ptr(), ctypes.byref(g), ctypes.byref(p),
+                                        stats.data_ptr(), codes.data_ptr(), outl.data_ptr(),
+                                        counts.data_ptr(), scalars.data_ptr(), res.data_ptr(),
+                                        wspace.data_ptr(), wsb, sp)
+        assert rc == 0
+        if ws > 1:  # per-shard outlier totals -> global offsets (metadata)
+            dist.all_gather_into_tensor(totals, res[2:3])
+        if timed:
+            ev[1].record(stream)
+        n_out = int(res[2].item())  # decompress takes the outlier count from the host
+        rc = lib.vlz_dq_decompress(codes.data_ptr(), outl.data_ptr(), n_out, counts.data_ptr(),
+                                   scalars.data_ptr(), ctypes.byref(g), ctypes.byref(p),
+                                   y.data_ptr(), dres.data_ptr(), wspace.data_ptr(), wsb, sp)
+        assert rc == 0
+        if timed:
+            ev[2].record(stream)
+            ev[2].synchronize()
+            t_c[0] += ev[0].elapsed_time(ev[1])
+            t_d[0] += ev[1].elapsed_time(ev[2])
+        return n_out
+
+    for _ in range(args.warmup):
+        n_out = step(False)
+    torch.cuda.synchronize()
+    r = _lib.Result()
+    rbuf = res.cpu().numpy()
+    ctypes.memmove(ctypes.byref(r), rbuf.ctypes.data, 64)
+    assert r.status == 0, f"compress status {r.status}"
+    rd = _lib.Result()
+    dbuf = dres.cpu().numpy()
+    ctypes.memmove(ctypes.byref(rd), dbuf.ctypes.data, 64)
+    assert rd.status == 0, f"decompress status {rd.status}"
+    # the round trip is exact: |y - x| <= eb everywhere
+    err = (y.double() - x.double()).abs().max().item()
+    assert err <= eb, f"bound violated {err} > {eb}"
+
+    clocks = ClockSampler(local)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = lib.vlz_launch_count()
+    lib.vlz_timing(1)
+    clocks.start()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        n_out = step(True)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    lib.vlz_timing(0)
+    launches = lib.vlz_launch_count() - l0
+    kms = (ctypes.c_double * 6)()
+    kcnt = (ctypes.c_int64 * 6)()
+    lib.vlz_timing_collect(kms, kcnt, 6)
+    elapsed = t0.elapsed_time(t1)
+    # per-phase compute time excludes the host sync for n_out; report both
+    tt = torch.tensor([elapsed, t_c[0], t_d[0], kms[1], kms[4], launches], dtype=torch.float64,
+                      device=dev)
+    if ws > 1:
+        mx = tt.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = tt.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        tt[:5] = mx[:5]
+        tt[5] = sm[5]
+        ntot = torch.tensor([n_out], dtype=torch.int64, device=dev)
+        dist.all_reduce(ntot)
+        n_out_total = int(ntot.item())
+    else:
+        n_out_total = n_out
+    elapsed, tc, td, k1, k4, launches = tt.tolist()
+    K = args.steps
+    N_total = D0 * SHAPE[1] * SHAPE[2]
+    in_bytes = 4.0 * N_total
+    value = in_bytes * K / (elapsed * 1e-3) / 1e9
+    peak, peak_kind = hbm_peak()
+
+    # roofline of the dominant kernel (per launch, this rank's shard)
+    nb = grid.block_count
+    alg = 6.0 * n + 4.0 * n_out + 8.0 * nb + 8.0
+    dom = "compress" if k1 >= k4 else "decompress"
+    kt = (k1 if dom == "compress" else k4) / K
+    achieved = alg / (kt * 1e-3) / 1e9
+    traffic = load_traffic(dom)
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = measure_e2e(args, x, eb, cfg, ws, rank, dev)
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        sample = x[:CPU_PLANES].cpu().numpy()
+        oracle_round_trip(sample, eb, threads)
+        ts = [oracle_round_trip(sample, eb, threads) for _ in range(3)]
+        cpu = {"value": 4.0 * sample.size / statistics.median(ts) / 1e9, "unit": "GB/s",
+               "cores": threads, "kind": "port",
+               "sample": f"C5 slab {sample.shape[0]}x{SHAPE[1]}x{SHAPE[2]} ({sample.size} elements),"
+                         f" CPU oracle compress+decompress, median of 3"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws, "steps": K,
+            "warmup": args.warmup, "ms_per_step": elapsed / K, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64+int32",
+            "data": "synthetic (C5 recipe: 64 seeded 3D sinusoidal modes + N(0,1e-3), on device)",
+            "config": workload_config(ws, eb),
+            "compress_gbs": in_bytes / (tc / K * 1e-3) / 1e9,
+            "decompress_gbs": in_bytes / (td / K * 1e-3) / 1e9,
+            "kernel_ms_per_step": {"fused_compress": k1 / K, "fused_decompress": k4 / K,
+                                   "compress_scan_gather": kms[2] / K, "decompress_scan": kms[3] / K,
+                                   "init": kms[0] / K},
+            "n_outliers": n_out_total,
+            "roofline": {"bound": "hbm", "kernel": f"fused_{dom}", "achieved": achieved,
+                         "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "algorithmic_bytes_per_launch": alg},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def load_traffic(kernel):
+    """dram bytes per launch of the kernel from the committed ncu summary."""
+    p = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return d.get(f"fused_{kernel}")
+    except Exception:
+        return None
+
+
+def measure_e2e(args, x, eb, cfg, ws, rank, dev):
+    """Host-buffer C-ABI round trip on a 2 GiB slab of this rank's shard."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2201_04614_b200 import _lib
+
+    lib = _lib.load()
+    planes = min(x.shape[0], 256)
+    sub = x[:planes].contiguous()
+    h_in = torch.empty(sub.shape, dtype=torch.float32, pin_memory=True)
+    h_in.copy_(sub)
+    n = sub.numel()
+    pol = cfg.padding
+    from paper_2201_04614_b200 import model as M
+
+    grid = M.build_block_grid(M.ArrayDescriptor(3, tuple(sub.shape)), BLOCK)
+    g = _lib.geom(sub.shape, BLOCK)
+    p = _lib.params(eb, RADIUS, pol.kind_code, pol.gran_code)
+    h_codes = torch.empty(n, dtype=torch.int16, pin_memory=True)
+    h_out = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    h_cnt = torch.empty(grid.block_count, dtype=torch.int64, pin_memory=True)
+    h_sc = torch.empty(1, dtype=torch.int64, pin_memory=True)
+    h_back = torch.empty(sub.shape, dtype=torch.float32, pin_memory=True)
+    r = _lib.Result()
+    rd = _lib.Result()
+    devi = dev.index
+
+    def one():
+        rc = lib.vlz_dq_compress_host(h_in.data_ptr(), ctypes.byref(g), ctypes.byref(p),
+                                      h_codes.data_ptr(), h_out.data_ptr(), h_cnt.data_ptr(),
+                                      h_sc.data_ptr(), ctypes.byref(r), devi)
+        assert rc == 0 and r.status == 0
+        rc = lib.vlz_dq_decompress_host(h_codes.data_ptr(), h_out.data_ptr(), r.n_outliers,
+                                        h_cnt.data_ptr(), h_sc.data_ptr(), ctypes.byref(g),
+                                        ctypes.byref(p), h_back.data_ptr(), ctypes.byref(rd), devi)
+        assert rc == 0 and rd.status == 0
+        return r.n_outliers
+
+    for _ in range(max(1, args.warmup)):
+        one()
+    steps = max(3, min(args.steps, 10))
+    if ws > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        n_out = one()
+    dt = time.perf_counter() - t0
+    t = torch.tensor([dt], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dt = float(t.item())
+    lib.vlz_host_release()
+    nb = grid.block_count
+    h2d = 4 * n + (2 * n + 4 * n_out + 8 * nb + 8)
+    d2h = (2 * n + 4 * n_out + 8 * nb + 8 + 64) + (4 * n + 64)
+    return {"value": 4.0 * n * ws * steps / dt / 1e9, "unit": "GB/s",
+            "h2d_bytes_per_step": int(h2d * ws), "d2h_bytes_per_step": int(d2h * ws),
+            "api": "vlz_dq_compress_host + vlz_dq_decompress_host (pinned host buffers)",
+            "sample": f"{planes}x{SHAPE[1]}x{SHAPE[2]} slab per rank, {steps} steps"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -163,6 +163,13 @@ void vlz_host_release(void);
 
 /* number of kernel launches the library issued since load (bench evidence) */
 int64_t vlz_launch_count(void);
+/* per-kernel CUDA-event timing: when enabled every launch is bracketed by
+ * events on its stream; collect() synchronises and returns, per kind
+ * (0 init, 1 fused compress, 2 compress scan/gather, 3 decompress scan,
+ * 4 fused decompress, 5 minmax), the summed milliseconds and launch counts
+ * since the last collect. */
+void vlz_timing(int enable);
+int vlz_timing_collect(double* ms, int64_t* launches, int n);
 /* library build string (arch, commit) */
 const char* vlz_version(void);
 

@@ -129,25 +129,30 @@ static inline int64_t flat_index(const grid_t* g, const int64_t* idx) {
  * overflow guard in row-major order; returns the first offending index. */
 int vlzo_prequantize(const float* data, int64_t n, double eb, int64_t* dq,
                      int64_t* err_index) {
-  if (!(eb > 0.0)) {
-    /* quantize.py:58-59 raises for eb <= 0; NaN eb falls through there and
-     * later trips the non-finite path only if the data is non-finite. */
-    if (eb <= 0.0) return VLZO_BAD_CONFIG;
-  }
-  for (int64_t i = 0; i < n; ++i) {
-    if (!isfinite(data[i])) {
-      *err_index = i;
-      return VLZO_NONFINITE;
-    }
+  if (eb <= 0.0) return VLZO_BAD_CONFIG; /* quantize.py:58-59 (NaN falls through) */
+  int64_t first_bad = INT64_MAX;
+#pragma omp parallel for reduction(min : first_bad) schedule(static)
+  for (int64_t i = 0; i < n; ++i)
+    if (!isfinite(data[i]) && i < first_bad) first_bad = i;
+  if (first_bad != INT64_MAX) {
+    *err_index = first_bad;
+    return VLZO_NONFINITE;
   }
   const double twoeb = 2.0 * eb;
+  int64_t first_ovf = INT64_MAX;
+#pragma omp parallel for reduction(min : first_ovf) schedule(static)
   for (int64_t i = 0; i < n; ++i) {
     double q = (double)data[i] / twoeb;
     if (fabs(q) >= OVERFLOW_LIMIT || q != q) {
-      *err_index = i;
-      return VLZO_OVERFLOW;
+      if (i < first_ovf) first_ovf = i;
+      dq[i] = 0;
+    } else {
+      dq[i] = round_half_away(q);
     }
-    dq[i] = round_half_away(q);
+  }
+  if (first_ovf != INT64_MAX) {
+    *err_index = first_ovf;
+    return VLZO_OVERFLOW;
   }
   return VLZO_OK;
 }
@@ -207,9 +212,16 @@ static void compute_padding(const grid_t* g, const int64_t* dq, int kind, int gr
   int64_t n = 1;
   for (int d = 0; d < g->nd; ++d) n *= g->dims[d];
   if (gran == GRAN_GLOBAL) {
-    stat_t s;
-    stat_reset(&s);
-    for (int64_t i = 0; i < n; ++i) stat_add(&s, dq[i]);
+    /* the int64 sum wraps like numpy's; unsigned addition is associative */
+    uint64_t sum = 0;
+    int64_t mn = INT64_MAX, mx = INT64_MIN;
+#pragma omp parallel for reduction(+ : sum) reduction(min : mn) reduction(max : mx) schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
+      sum += (uint64_t)dq[i];
+      if (dq[i] < mn) mn = dq[i];
+      if (dq[i] > mx) mx = dq[i];
+    }
+    stat_t s = {mn, mx, sum, n};
     scalars[0] = stat_value(&s, kind);
     return;
   }
@@ -287,6 +299,19 @@ static inline int64_t lorenzo_predict(const padded_t* p, int64_t i, int64_t j, i
          value_at(p, i - 1, j - 1, k) + value_at(p, i - 1, j - 1, k - 1);
 }
 
+/* grow-only scratch arena (not re-entrant: the oracle is called serially) */
+static void* g_arena = NULL;
+static size_t g_arena_cap = 0;
+
+static void* arena_get(size_t bytes) {
+  if (bytes > g_arena_cap) {
+    free(g_arena);
+    g_arena = malloc(bytes);
+    g_arena_cap = g_arena ? bytes : 0;
+  }
+  return g_arena;
+}
+
 /* closed-form canonical start of a block's codes (sum of sizes of all
  * earlier blocks in row-major block order) */
 static int64_t block_code_start(const grid_t* g, int64_t bi) {
@@ -329,19 +354,16 @@ int vlzo_dualquant(const float* data, int nd, const int64_t* dims, int b, double
   grid_init(&g, nd, dims, b);
   int64_t n = 1;
   for (int d = 0; d < nd; ++d) n *= dims[d];
-  int64_t* dq = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
-  float* scratch = (float*)malloc(sizeof(float) * (size_t)(n > 0 ? n : 1));
-  if (!dq || !scratch) {
-    free(dq);
-    free(scratch);
-    return VLZO_NOMEM;
-  }
+  /* dq + scratch come from a grow-only arena: re-faulting hundreds of MB of
+   * fresh pages per call serialises on the kernel's mm lock and would make
+   * the CPU baseline measure page faults instead of the algorithm */
+  const size_t nn = (size_t)(n > 0 ? n : 1);
+  char* arena = (char*)arena_get(nn * (sizeof(int64_t) + sizeof(float)));
+  if (!arena) return VLZO_NOMEM;
+  int64_t* dq = (int64_t*)arena;
+  float* scratch = (float*)(arena + nn * sizeof(int64_t));
   int rc = vlzo_prequantize(data, n, eb, dq, err_index);
-  if (rc != VLZO_OK) {
-    free(dq);
-    free(scratch);
-    return rc;
-  }
+  if (rc != VLZO_OK) return rc;
   compute_padding(&g, dq, pad_kind, pad_gran, scalars);
   const int64_t keep_max = radius - 1;
   const int64_t bmax = (int64_t)b * (nd > 1 ? b : 1) * (nd > 2 ? b : 1);
@@ -402,8 +424,6 @@ int vlzo_dualquant(const float* data, int nd, const int64_t* dims, int b, double
     }
   }
   *n_out = off;
-  free(dq);
-  free(scratch);
   return VLZO_OK;
 }
 
@@ -430,6 +450,7 @@ int vlzo_reconstruct(const uint32_t* codes, const float* outlier_vals, int64_t n
   for (int d = 0; d < nd; ++d) n *= dims[d];
   /* reconstruct.py:87-91: sentinel total must equal the outlier count */
   int64_t nsent = 0;
+#pragma omp parallel for reduction(+ : nsent) schedule(static)
   for (int64_t i = 0; i < n; ++i) nsent += codes[i] == 0;
   if (nsent != n_out) {
     *err_index = nsent;

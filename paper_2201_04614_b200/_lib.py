@@ -64,6 +64,8 @@ PROTOTYPES = {
                                               _P(Result), ctypes.c_int]),
     "vlz_host_release": (None, []),
     "vlz_launch_count": (_i64, []),
+    "vlz_timing": (None, [ctypes.c_int]),
+    "vlz_timing_collect": (ctypes.c_int, [_P(ctypes.c_double), _P(_i64), ctypes.c_int]),
     "vlz_version": (ctypes.c_char_p, []),
 }
 

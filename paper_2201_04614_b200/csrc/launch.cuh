@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <type_traits>
 
 #include "dq_decompress.cuh"
 
@@ -13,6 +14,12 @@ namespace vlz {
 extern std::atomic<long long> g_launches;
 
 int num_sms();
+
+// optional per-kernel CUDA-event timing (vlz_timing / vlz_timing_collect)
+enum TimedKind { TK_INIT = 0, TK_COMPRESS = 1, TK_SCAN_C = 2, TK_SCAN_D = 3, TK_DECOMPRESS = 4,
+                 TK_MINMAX = 5, TK_COUNT = 6 };
+extern std::atomic<int> g_timing;
+void timing_mark(int kind, bool start, cudaStream_t st);
 
 // grid = min(resident CTAs, tiles/4) for a 128-thread warp-per-tile kernel
 template <typename Kern, typename Arg>
@@ -30,7 +37,10 @@ inline cudaError_t launch_tiles(Kern kernel, int64_t ntiles, int smem, cudaStrea
   const int64_t need = (ntiles + 3) / 4;
   if (grid > need) grid = need;
   if (grid < 1) grid = 1;
+  const int kind = std::is_same<Arg, CompressArgs>::value ? TK_COMPRESS : TK_DECOMPRESS;
+  if (g_timing.load(std::memory_order_relaxed)) timing_mark(kind, true, st);
   kernel<<<(unsigned)grid, 128, smem, st>>>(arg);
+  if (g_timing.load(std::memory_order_relaxed)) timing_mark(kind, false, st);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }

@@ -21,6 +21,40 @@
 namespace vlz {
 
 std::atomic<long long> g_launches{0};
+std::atomic<int> g_timing{0};
+
+namespace {
+struct TimedRec {
+  int kind;
+  cudaEvent_t a, b;
+};
+std::mutex g_tmu;
+std::vector<TimedRec> g_trecs;
+std::vector<cudaEvent_t> g_epool;
+cudaEvent_t g_open[TK_COUNT];
+
+cudaEvent_t take_event() {
+  if (!g_epool.empty()) {
+    cudaEvent_t e = g_epool.back();
+    g_epool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+}  // namespace
+
+void timing_mark(int kind, bool start, cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(g_tmu);
+  cudaEvent_t e = take_event();
+  cudaEventRecord(e, st);
+  if (start) {
+    g_open[kind] = e;
+  } else {
+    g_trecs.push_back({kind, g_open[kind], e});
+  }
+}
 
 int num_sms() {
   static int n = 0;
@@ -148,7 +182,10 @@ cudaError_t launch_init(vlz_result* res, const WS& w, long long* stats, int64_t 
   int64_t blocks = (nchunks + 255) / 256;
   if (blocks < 1) blocks = 1;
   if (blocks > 1024) blocks = 1024;
+  const bool t = g_timing.load(std::memory_order_relaxed);
+  if (t) timing_mark(TK_INIT, true, st);
   init_kernel<<<(unsigned)blocks, 256, 0, st>>>(res, w.ticket, w.done, stats, w.lb, nchunks);
+  if (t) timing_mark(TK_INIT, false, st);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
@@ -156,7 +193,11 @@ cudaError_t launch_init(vlz_result* res, const WS& w, long long* stats, int64_t 
 cudaError_t launch_scan(const ScanArgs& a, cudaStream_t st) {
   int64_t nchunks = (a.g.nblocks + SCAN_CH - 1) / SCAN_CH;
   if (nchunks < 1) nchunks = 1;
+  const bool t = g_timing.load(std::memory_order_relaxed);
+  const int kind = a.gather ? TK_SCAN_C : TK_SCAN_D;
+  if (t) timing_mark(kind, true, st);
   dq_scan_kernel<<<(unsigned)nchunks, SCAN_THREADS, 0, st>>>(a);
+  if (t) timing_mark(kind, false, st);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
@@ -587,6 +628,29 @@ void vlz_host_release(void) {
 }
 
 int64_t vlz_launch_count(void) { return g_launches.load(); }
+
+void vlz_timing(int enable) { g_timing.store(enable ? 1 : 0); }
+
+int vlz_timing_collect(double* ms, int64_t* launches, int n) {
+  std::lock_guard<std::mutex> lk(g_tmu);
+  for (int k = 0; k < n; ++k) {
+    ms[k] = 0.0;
+    launches[k] = 0;
+  }
+  for (const TimedRec& r : g_trecs) {
+    float t = 0.f;
+    cudaEventSynchronize(r.b);
+    cudaEventElapsedTime(&t, r.a, r.b);
+    if (r.kind < n) {
+      ms[r.kind] += t;
+      launches[r.kind] += 1;
+    }
+    g_epool.push_back(r.a);
+    g_epool.push_back(r.b);
+  }
+  g_trecs.clear();
+  return VLZ_OK;
+}
 
 const char* vlz_version(void) { return "vlz_gpu 0.1 sm_100a"; }
 

@@ -118,27 +118,66 @@ def value_range_eb(data: np.ndarray, rel: float) -> float:
 
 
 def gen_modes_torch(shape, count, kmax, power, noise, seed, device, z_range=None):
-    """Mode-sum field generated on the GPU, optionally only planes z_range."""
+    """3-D mode-sum field (C5 recipe) for planes z_range of `shape`, built on
+    the GPU: per mode one 2-D float64 phase plane, then float32 broadcast
+    multiply-adds over the slab.  Deterministic for a given (seed, z_range)."""
     import torch
 
     rng = np.random.default_rng(seed)
-    nd = len(shape)
-    ks, phase, amp = _modes(rng, nd, count, kmax, power)
-    z0, z1 = z_range if z_range is not None else (0, shape[0])
-    out = torch.empty((z1 - z0,) + tuple(shape[1:]), dtype=torch.float32, device=device)
+    ks, phase, amp = _modes(rng, 3, count, kmax, power)
+    D0, D1, D2 = shape
+    z0, z1 = z_range if z_range is not None else (0, D0)
+    out = torch.zeros((z1 - z0, D1, D2), dtype=torch.float32, device=device)
+    zz = torch.arange(z0, z1, dtype=torch.float64, device=device) / D0
+    yy = torch.arange(D1, dtype=torch.float64, device=device) / D1
+    xx = torch.arange(D2, dtype=torch.float64, device=device) / D2
+    for m in range(count):
+        a = 2.0 * math.pi * float(ks[m, 0]) * zz + float(phase[m])
+        inner = (2.0 * math.pi * float(ks[m, 1]) * yy)[:, None] + (
+            2.0 * math.pi * float(ks[m, 2]) * xx
+        )[None, :]
+        cb, sb = torch.cos(inner).float(), torch.sin(inner).float()
+        sa = (float(amp[m]) * torch.sin(a)).float()
+        ca = (float(amp[m]) * torch.cos(a)).float()
+        out.addcmul_(sa[:, None, None], cb[None])
+        out.addcmul_(ca[:, None, None], sb[None])
     gen = torch.Generator(device=device)
-    gen.manual_seed(seed * 7919 + z0)
-    axes = [torch.arange(s, dtype=torch.float64, device=device) / s for s in shape]
-    for p in range(z0, z1):
-        acc = torch.zeros(tuple(shape[1:]), dtype=torch.float64, device=device)
-        for m in range(count):
-            arg = 2.0 * math.pi * float(ks[m, 0]) * float(axes[0][p]) + float(phase[m])
-            if nd == 2:
-                acc += float(amp[m]) * torch.sin(arg + 2.0 * math.pi * float(ks[m, 1]) * axes[1])
-            else:
-                a1 = 2.0 * math.pi * float(ks[m, 1]) * axes[1]
-                a2 = 2.0 * math.pi * float(ks[m, 2]) * axes[2]
-                acc += float(amp[m]) * torch.sin(arg + a1[:, None] + a2[None, :])
-        out[p - z0] = acc.float()
-    out += torch.randn(out.shape, generator=gen, device=device, dtype=torch.float32) * noise
+    gen.manual_seed(seed * 1_000_003 + z0)
+    step = max(1, (1 << 28) // (D1 * D2))
+    for p in range(0, z1 - z0, step):
+        sl = out[p:p + step]
+        sl.add_(torch.randn(sl.shape, generator=gen, device=device, dtype=torch.float32), alpha=noise)
+    return out
+
+
+def gen_c5_slab(z_range, device, shape=(2048, 2048, 1024), seed: int = 5):
+    """BASELINE config 5 (64 modes, k in [1,16]^3, amp 1/|k|, + N(0,1e-3))."""
+    return gen_modes_torch(shape, 64, 16, 1.0, 1e-3, seed, device, z_range)
+
+
+def gen_c5_slab_numpy(z_range, shape=(2048, 2048, 1024), seed: int = 5) -> np.ndarray:
+    """CPU (float64) build of the C5 recipe for a slab -- used by the
+    reference arm of bench.py, which must not touch the GPU path.  The 2-D
+    phase plane e^{i(b+c)} is the outer product of two 1-D exponentials."""
+    rng = np.random.default_rng(seed)
+    ks, phase, amp = _modes(rng, 3, 64, 16, 1.0)
+    D0, D1, D2 = shape
+    z0, z1 = z_range
+    zz, yy, xx = np.arange(z0, z1) / D0, np.arange(D1) / D1, np.arange(D2) / D2
+    acc = np.zeros((z1 - z0, D1, D2), dtype=np.float64)
+    t2 = np.empty((D1, D2), dtype=np.float64)
+    for m in range(64):
+        a = 2.0 * math.pi * ks[m, 0] * zz + phase[m]
+        b = 2.0 * math.pi * ks[m, 1] * yy
+        c = 2.0 * math.pi * ks[m, 2] * xx
+        re = np.outer(np.cos(b), np.cos(c)) - np.outer(np.sin(b), np.sin(c))
+        im = np.outer(np.sin(b), np.cos(c)) + np.outer(np.cos(b), np.sin(c))
+        sa, ca = amp[m] * np.sin(a), amp[m] * np.cos(a)
+        for p in range(z1 - z0):
+            np.multiply(re, sa[p], out=t2)
+            acc[p] += t2
+            np.multiply(im, ca[p], out=t2)
+            acc[p] += t2
+    out = acc.astype(np.float32)
+    out += np.random.default_rng(seed * 1_000_003 + z0).normal(0.0, 1e-3, out.shape).astype(np.float32)
     return out
