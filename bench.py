@@ -307,9 +307,9 @@ def run_ours(args):
     clk = clocks.stop()
     lib.vlz_timing(0)
     launches = lib.vlz_launch_count() - l0
-    kms = (ctypes.c_double * 6)()
-    kcnt = (ctypes.c_int64 * 6)()
-    lib.vlz_timing_collect(kms, kcnt, 6)
+    kms = (ctypes.c_double * 8)()
+    kcnt = (ctypes.c_int64 * 8)()
+    lib.vlz_timing_collect(kms, kcnt, 8)
     elapsed = t0.elapsed_time(t1)
     # per-phase compute time excludes the host sync for n_out; report both
     tt = torch.tensor([elapsed, t_c[0], t_d[0], kms[1], kms[4], launches], dtype=torch.float64,

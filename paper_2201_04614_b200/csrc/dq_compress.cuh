@@ -49,6 +49,9 @@ struct CompressArgs {
   unsigned long long* gcount;
   long long* gmin;
   long long* gnegmax;
+  // int64 redo list written by the fast kernel (tile ids)
+  const unsigned int* redo_count;
+  const long long* redo_list;
 };
 
 // per-warp statistics for MODE_GLOBAL (lane partials)
@@ -338,7 +341,10 @@ __device__ __forceinline__ bool compress_tile(const CompressArgs& a, int64_t til
   return false;
 }
 
-template <int ND, int B, int VPL, int MODE>
+// LIST = false: every tile (uint32 stencil, int64 redo on demand).
+// LIST = true : only the tiles the fast kernel appended to the redo list,
+//               directly in int64 (dq_compress_fast.cuh).
+template <int ND, int B, int VPL, int MODE, bool LIST = false>
 __global__ void __launch_bounds__(128) dq_compress_kernel(CompressArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int PB = plane_smem_bytes<ND, B, VPL>();
@@ -347,12 +353,16 @@ __global__ void __launch_bounds__(128) dq_compress_kernel(CompressArgs a) {
   unsigned char* wsm = smem_raw + (size_t)wib * PB;
   GlobalAcc gacc;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t tile = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib; tile < a.g.ntiles;
-       tile += nwarps) {
-    if (compress_tile<ND, B, VPL, MODE, unsigned>(a, tile, lane,
-                                                  reinterpret_cast<unsigned*>(wsm), gacc))
-      compress_tile<ND, B, VPL, MODE, long long>(a, tile, lane,
+  const int64_t ntodo = LIST ? (int64_t)*a.redo_count : a.g.ntiles;
+  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib; i < ntodo; i += nwarps) {
+    if (LIST) {
+      compress_tile<ND, B, VPL, MODE, long long>(a, a.redo_list[i], lane,
                                                  reinterpret_cast<long long*>(wsm), gacc);
+    } else if (compress_tile<ND, B, VPL, MODE, unsigned>(a, i, lane,
+                                                         reinterpret_cast<unsigned*>(wsm), gacc)) {
+      compress_tile<ND, B, VPL, MODE, long long>(a, i, lane,
+                                                 reinterpret_cast<long long*>(wsm), gacc);
+    }
   }
   if (MODE == MODE_GLOBAL) {
     // warp reduce, then one atomic set per warp

@@ -1,0 +1,498 @@
+// dq_compress_fast.cuh -- the production fused compress kernel (sm_100a).
+//
+// Same tile decomposition and output contract as dq_compress.cuh (one warp per
+// tile = one block layer x one block row x a window of W = 32*VPL columns),
+// specialised for the throughput-critical shapes (3-D b=8/16, 2-D b=8/16):
+//
+//  * input planes (BY rows x W floats, 4 KB) stream into a per-warp shared-
+//    memory ring with TMA bulk copies (cp.async.bulk + mbarrier complete_tx),
+//    FAST_STAGES planes ahead of the compute and across tile boundaries; each
+//    lane reads its VPL columns of a row with one vector LDS;
+//  * prequantization runs the float32 fast path (vlz_common.cuh quant_fast)
+//    and re-evaluates only flagged elements with the exact float64 rules;
+//  * the Lorenzo stencil runs in int32 (every |d| of the tile < 2^24); a tile
+//    holding a larger |d| is appended to a redo list and recomputed in int64 by
+//    dq_compress_kernel<..., LIST=true>; such a tile commits nothing here;
+//  * interior tiles (whole window inside the row, full block rows) take a
+//    branch-free specialisation with constant code strides;
+//  * tile ids are decoded with 32-bit magic division, ring slots advance
+//    incrementally -- per-plane overhead is a handful of instructions.
+// Origin deferral, padding statistics, outlier slots and error minima are
+// identical to dq_compress.cuh.
+#pragma once
+
+#include "dq_compress.cuh"
+#include "tma.cuh"
+
+namespace vlz {
+
+constexpr int FAST_STAGES = 2;
+constexpr int FAST_WARPS = 4;
+
+template <int ND, int B, int VPL>
+struct FastShape {
+  using S = Shape<ND, B, VPL>;
+  static constexpr int PLANE_FLOATS = S::BY * S::W;
+  static constexpr int PLANE_BYTES = PLANE_FLOATS * 4;
+  // ring of input planes + the previous plane's Dy Dx d (int32, 3-D only)
+  static constexpr int PREV_BYTES = (ND == 3) ? PLANE_BYTES : 0;
+  static constexpr int WARP_SMEM = FAST_STAGES * PLANE_BYTES + PREV_BYTES + 64;
+};
+
+template <int ND, int B, int VPL>
+__host__ __device__ constexpr int fast_smem_bytes() {
+  return FAST_WARPS * FastShape<ND, B, VPL>::WARP_SMEM;
+}
+
+struct FastArgs {
+  CompressArgs c;
+  unsigned int* redo_count;
+  long long* redo_list;
+};
+
+struct TileXY {
+  uint32_t wx, by, bz;
+};
+
+__device__ __forceinline__ TileXY decode_tile(const Geo& g, uint32_t tile) {
+  TileXY t;
+  const uint32_t t2 = g.divNW.div(tile);
+  t.wx = tile - t2 * (uint32_t)g.NW;
+  t.bz = g.divP1.div(t2);
+  t.by = t2 - t.bz * (uint32_t)g.P1;
+  return t;
+}
+
+// producer side of the per-warp plane ring
+template <int ND, int B, int VPL>
+struct Producer {
+  using S = Shape<ND, B, VPL>;
+  uint32_t tile;       // current tile (>= ntiles: done)
+  int zl, ez, ey;
+  const float* src;    // first row of the current plane
+  uint32_t row_bytes;
+  int stage;
+
+  __device__ __forceinline__ void start(const Geo& g, const float* in, uint32_t t) {
+    tile = t;
+    zl = 0;
+    stage = 0;
+    setup(g, in);
+  }
+  __device__ __forceinline__ void setup(const Geo& g, const float* in) {
+    if (tile >= (uint32_t)g.ntiles) return;
+    const TileXY c = decode_tile(g, tile);
+    const int64_t z0 = (int64_t)c.bz * S::BZ, y0 = (int64_t)c.by * S::BY;
+    const int64_t x0 = (int64_t)c.wx * S::W;
+    ez = (int)imin64(S::BZ, g.D0 - z0);
+    ey = (int)imin64(S::BY, g.D1 - y0);
+    row_bytes = (uint32_t)imin64(S::W, g.D2 - x0) * 4u;
+    src = in + (z0 * g.D1 + y0) * g.D2 + x0;
+  }
+  // issue the current plane into `stage`, then advance (all lanes call)
+  __device__ __forceinline__ void issue(const Geo& g, const float* in, float* ring,
+                                        uint64_t* bars, int lane, uint32_t nwarps) {
+    using F = FastShape<ND, B, VPL>;
+    if (tile >= (uint32_t)g.ntiles) return;
+    float* buf = ring + stage * F::PLANE_FLOATS;
+    uint64_t* bar = &bars[stage];
+    if (lane == 0) mbar_arrive_expect_tx(bar, row_bytes * (uint32_t)ey);
+    __syncwarp();
+    if (lane < ey) bulk_g2s(buf + lane * S::W, src + (int64_t)lane * g.D2, row_bytes, bar);
+    if (++stage == FAST_STAGES) stage = 0;
+    if (++zl < ez) {
+      src += g.D1 * g.D2;
+    } else {
+      zl = 0;
+      tile += nwarps;
+      setup(g, in);
+    }
+  }
+};
+
+template <int ND, int B, int VPL>
+struct Consumer {
+  int stage;
+  uint32_t parity;
+  __device__ __forceinline__ void advance() {
+    if (++stage == FAST_STAGES) {
+      stage = 0;
+      parity ^= 1u;
+    }
+  }
+};
+
+
+// statistic accumulator for a compile-time padding kind K (1 min, 2 max, 3 mean)
+template <int K>
+struct KAcc {
+  long long sum = 0;
+  int mn = 0x7fffffff, mx = (int)0x80000000;
+  __device__ __forceinline__ void add(int v) {
+    if (K == 3) sum += v;
+    if (K == 1) mn = v < mn ? v : mn;
+    if (K == 2) mx = v > mx ? v : mx;
+  }
+  __device__ __forceinline__ void merge(const KAcc& o) {
+    sum += o.sum;
+    mn = o.mn < mn ? o.mn : mn;
+    mx = o.mx > mx ? o.mx : mx;
+  }
+};
+
+// One tile.  INTERIOR: x window fully inside the array and ey == BY, so all
+// lanes hold VPL in-bounds columns of full-width blocks.  K = padding kind
+// for the statistics (compile time; ignored for MODE_ZERO).
+template <int ND, int B, int VPL, int MODE, int K, bool INTERIOR>
+__device__ __forceinline__ void fast_tile(const FastArgs& fa, uint32_t tile, const TileXY& tc,
+                                          int lane, float* ring, uint64_t* bars,
+                                          Producer<ND, B, VPL>& prod, Consumer<ND, B, VPL>& cons,
+                                          uint32_t nwarps, KAcc<K>& gacc, long long& gcnt) {
+  using S = Shape<ND, B, VPL>;
+  using F = FastShape<ND, B, VPL>;
+  constexpr int BZ = S::BZ, BY = S::BY, BX = S::BX, W = S::W, LPB = S::LPB;
+  constexpr unsigned MAGIC_BITS = 0x4B400000u;  // bit pattern of 1.5 * 2^23
+  const CompressArgs& a = fa.c;
+  const Geo& g = a.g;
+  const QP& q = a.q;
+  const int R = q.radius;
+  const unsigned span = (unsigned)(2 * R - 2);  // in range iff (delta + R - 1) <= 2R - 2
+
+  const int64_t z0 = (int64_t)tc.bz * BZ, y0 = (int64_t)tc.by * BY;
+  const int ez = (int)imin64(BZ, g.D0 - z0);
+  const int ey = INTERIOR ? BY : (int)imin64(BY, g.D1 - y0);
+  const int64_t xl0 = (int64_t)tc.wx * W + lane * VPL;
+  const int xin = (lane * VPL) % BX;
+  const int nvalid = INTERIOR ? VPL : (int)imax64(0, imin64(VPL, g.D2 - xl0));
+  const bool lane_valid = INTERIOR || nvalid > 0;
+  const int64_t bxg = xl0 / BX;
+  const int ex = INTERIOR ? BX : (int)imax64(0, imin64(BX, g.D2 - bxg * BX));
+  const int64_t bi = ((int64_t)tc.bz * g.P1 + tc.by) * g.P2 + bxg;
+  const int64_t bstart = block_start(g, tc.bz, tc.by, bxg, BZ, BY, BX, ez, ey);
+  const bool vec_store = INTERIOR || ((nvalid == VPL) && (ex == BX));
+  const unsigned vmask = INTERIOR ? ((1u << VPL) - 1u) : ((1u << nvalid) - 1u);
+  // the x-difference at a block's first column reads the zero halo: feed the
+  // magic-number bias there so that the biased bit patterns cancel exactly
+  const bool xhead = (xin == 0);
+
+  int* const pplane = reinterpret_cast<int*>(ring + FAST_STAGES * F::PLANE_FLOATS) + lane * VPL;
+  if (ND == 3) {  // previous-plane state starts at zero (Dz zero fill)
+#pragma unroll 1
+    for (int yl = 0; yl < BY; ++yl) {
+      if (VPL == 4) *reinterpret_cast<int4*>(pplane + yl * W) = make_int4(0, 0, 0, 0);
+      else *reinterpret_cast<int2*>(pplane + yl * W) = make_int2(0, 0);
+    }
+  }
+  int run = 0;
+  bool wide = false;
+  int d_origin = 0;
+  bool bad_origin = false;
+  float v_origin = 0.f;
+  KAcc<K> tacc;
+  KAcc<K> face[ND];
+  long long tcnt = 0;
+  uint16_t* cptr = a.codes + bstart + xin;  // advances by ex per row
+
+  for (int zl = 0; zl < ez; ++zl) {
+    const float* plane = ring + cons.stage * F::PLANE_FLOATS + lane * VPL;
+    mbar_wait(&bars[cons.stage], cons.parity);
+    int prow[VPL];
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) prow[j] = 0;  // Dy zero fill at the block's first row
+    long long psum = 0;
+#pragma unroll 1
+    for (int yl = 0; yl < BY; ++yl) {
+      if (!INTERIOR && yl >= ey) break;
+      float v[VPL];
+      if (VPL == 4) {
+        const float4 f = *reinterpret_cast<const float4*>(plane + yl * W);
+        v[0] = f.x; v[1 % VPL] = f.y; v[2 % VPL] = f.z; v[3 % VPL] = f.w;
+      } else {
+        const float2 f = *reinterpret_cast<const float2*>(plane + yl * W);
+        v[0] = f.x; v[1 % VPL] = f.y;
+      }
+      // ---- float32 fast prequantization; nb = biased bit pattern of n
+      unsigned nb[VPL];
+      bool allok = true;
+#pragma unroll
+      for (int j = 0; j < VPL; ++j) {
+        const float qq = __fmul_rn(v[j], q.inv32);
+        const float r = __fadd_rn(qq, 12582912.0f);
+        nb[j] = __float_as_uint(r);
+        const float e = __fsub_rn(qq, __fsub_rn(r, 12582912.0f));
+        allok = allok && (fabsf(e) < __fmaf_rn(fabsf(qq), -q.kq, q.lim0));
+      }
+      if (!INTERIOR) {
+#pragma unroll
+        for (int j = 0; j < VPL; ++j)
+          if (j >= nvalid) nb[j] = MAGIC_BITS;  // out-of-bounds columns act as d = 0
+      }
+      bool bad[VPL];
+#pragma unroll
+      for (int j = 0; j < VPL; ++j) bad[j] = false;
+      if (!__all_sync(FULL, allok)) {
+        // rare: exact float64 re-evaluation of the flagged elements, one at a
+        // time (one inlined copy of quant_exact; operands picked by select)
+        unsigned sm = 0;
+#pragma unroll
+        for (int j = 0; j < VPL; ++j) {
+          bool ok;
+          quant_fast(v[j], q, ok);
+          if (!ok && (INTERIOR || j < nvalid)) sm |= 1u << j;
+        }
+        while (sm) {
+          const int j = __ffs(sm) - 1;
+          sm &= sm - 1;
+          float vj = v[0];
+#pragma unroll
+          for (int k = 1; k < VPL; ++k) vj = (j == k) ? v[k] : vj;
+          bool bj, ovf;
+          const int nj = quant_exact(vj, q, bj, ovf);
+#pragma unroll
+          for (int k = 0; k < VPL; ++k) {
+            nb[k] = (j == k) ? (unsigned)nj + MAGIC_BITS : nb[k];
+            bad[k] = (j == k) ? bj : bad[k];
+          }
+          if (ovf) {
+            const unsigned long long fi =
+                (unsigned long long)(((z0 + zl) * g.D1 + (y0 + yl)) * g.D2 + xl0 + j);
+            if (!isfinite(vj)) atomicMin(a.first_nonfinite, fi);
+            atomicMin(a.first_overflow, fi);
+          }
+          wide |= (nj >= (1 << 24)) || (nj <= -(1 << 24));
+        }
+      }
+      // ---- Dx, Dy, Dz in int32 (exact: |d| < 2^24 unless `wide`).  The bias
+      // cancels in every difference; the block head subtracts the bias itself.
+      unsigned left = __shfl_up_sync(FULL, nb[VPL - 1], 1);
+      if (xhead) left = MAGIC_BITS;
+      int dl[VPL];
+      dl[0] = (int)(nb[0] - left);
+#pragma unroll
+      for (int j = 1; j < VPL; ++j) dl[j] = (int)(nb[j] - nb[j - 1]);
+      if (ND >= 2) {
+#pragma unroll
+        for (int j = 0; j < VPL; ++j) {
+          const int t = dl[j] - prow[j];
+          prow[j] = dl[j];
+          dl[j] = t;
+        }
+      }
+      if (ND == 3) {
+        int* pp = pplane + yl * W;
+        int prev[VPL];
+        if (VPL == 4) {
+          const int4 p4 = *reinterpret_cast<const int4*>(pp);
+          prev[0] = p4.x; prev[1 % VPL] = p4.y; prev[2 % VPL] = p4.z; prev[3 % VPL] = p4.w;
+          *reinterpret_cast<int4*>(pp) = make_int4(dl[0], dl[1 % VPL], dl[2 % VPL], dl[3 % VPL]);
+        } else {
+          const int2 p2 = *reinterpret_cast<const int2*>(pp);
+          prev[0] = p2.x; prev[1 % VPL] = p2.y;
+          *reinterpret_cast<int2*>(pp) = make_int2(dl[0], dl[1 % VPL]);
+        }
+#pragma unroll
+        for (int j = 0; j < VPL; ++j) dl[j] -= prev[j];
+      }
+      // ---- postquantization: code = delta + R, or 0 for an outlier
+      bool out[VPL];
+      uint32_t c[VPL];
+      bool anyout = false;
+#pragma unroll
+      for (int j = 0; j < VPL; ++j) {
+        const int u = dl[j] + (R - 1);
+        out[j] = ((unsigned)u > span) || bad[j];
+        c[j] = out[j] ? 0u : (uint32_t)(u + 1);
+        anyout = anyout || out[j];
+      }
+      const bool origin_row = (zl == 0) && (yl == 0) && xhead;
+      if (origin_row) {
+        d_origin = (int)(nb[0] - MAGIC_BITS);
+        bad_origin = bad[0];
+        v_origin = v[0];
+      }
+      if (vec_store) {
+        if (VPL == 4) {
+          *reinterpret_cast<uint2*>(cptr) =
+              make_uint2(__byte_perm(c[0], c[1 % VPL], 0x5410), __byte_perm(c[2 % VPL], c[3 % VPL], 0x5410));
+        } else {
+          *reinterpret_cast<uint32_t*>(cptr) = __byte_perm(c[0], c[1 % VPL], 0x5410);
+        }
+      } else if (lane_valid) {
+#pragma unroll
+        for (int j = 0; j < VPL; ++j)
+          if (j < nvalid) cptr[j] = (uint16_t)c[j];
+      }
+      cptr += ex;
+      // ---- outliers (rare): rank inside the block in traversal order
+      if (__any_sync(FULL, anyout)) {
+        unsigned om = 0;
+#pragma unroll
+        for (int j = 0; j < VPL; ++j) om |= out[j] ? (1u << j) : 0u;
+        om &= vmask;
+        if (origin_row) om &= ~1u;
+        int tot;
+        const int excl = group_excl_scan<LPB>(__popc(om), lane, tot);
+        int k = run + excl;
+        float* slot = a.scratch + bstart + 1;
+#pragma unroll
+        for (int j = 0; j < VPL; ++j)
+          if ((om >> j) & 1u) slot[k++] = v[j];
+        run += tot;
+      }
+      // ---- padding statistics on d = nb - bias (in-bounds columns only)
+      if (MODE == MODE_GLOBAL) {
+        if (K == 3) {
+          unsigned rs = nb[0];
+#pragma unroll
+          for (int j = 1; j < VPL; ++j) rs += nb[j];
+          psum += (int)(rs - (unsigned)VPL * MAGIC_BITS);  // out-of-bounds columns hold the bias
+        } else {
+#pragma unroll
+          for (int j = 0; j < VPL; ++j)
+            if (INTERIOR || j < nvalid) tacc.add((int)(nb[j] - MAGIC_BITS));
+        }
+      } else if (MODE == MODE_BLOCK) {
+#pragma unroll
+        for (int j = 0; j < VPL; ++j)
+          if (INTERIOR || j < nvalid) face[0].add((int)(nb[j] - MAGIC_BITS));
+      } else if (MODE == MODE_EDGE) {
+#pragma unroll
+        for (int j = 0; j < VPL; ++j) {
+          if (!INTERIOR && j >= nvalid) continue;
+          const int d = (int)(nb[j] - MAGIC_BITS);
+          const bool x0 = (xin + j) == 0;
+          if (ND == 3) {
+            if (zl == 0) face[0].add(d);
+            if (yl == 0) face[1 % ND].add(d);
+            if (x0) face[ND - 1].add(d);
+          } else {
+            if (yl == 0) face[0].add(d);
+            if (x0) face[ND - 1].add(d);
+          }
+        }
+      }
+    }
+    if (MODE == MODE_GLOBAL) {
+      tacc.sum += psum;
+      tcnt += (long long)nvalid * ey;
+    }
+    // release the slot and refill it FAST_STAGES planes ahead
+    __syncwarp();
+    fence_proxy_async_smem();
+    prod.issue(g, a.in, ring, bars, lane, nwarps);
+    cons.advance();
+  }
+
+  // int32 stencil may have wrapped: hand the whole tile to the int64 redo
+  if (__any_sync(FULL, wide)) {
+    if (lane == 0) fa.redo_list[atomicAdd(fa.redo_count, 1u)] = tile;
+    return;
+  }
+
+  // ---- tile end: padding scalars, block origins, counts (as dq_compress.cuh)
+  const bool group_lead = lane_valid && xhead;
+  int64_t s0 = 0;
+  if (MODE == MODE_BLOCK || MODE == MODE_EDGE) {
+    constexpr int NF = (MODE == MODE_BLOCK) ? 1 : ND;
+    const int64_t ext[3] = {ND == 3 ? (int64_t)ez : (int64_t)ey,
+                            ND == 3 ? (int64_t)ey : (int64_t)ex, (int64_t)ex};
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+      const int64_t sum = K == 3 ? group_sum<LPB>(face[f].sum) : 0;
+      const int mn = K == 1 ? group_min<LPB>(face[f].mn) : 0;
+      const int mx = K == 2 ? group_max<LPB>(face[f].mx) : 0;
+      int64_t cnt;
+      if (MODE == MODE_BLOCK) {
+        cnt = ext[0] * ext[1] * (ND == 3 ? ext[2] : 1);
+      } else {
+        cnt = 1;
+#pragma unroll
+        for (int d = 0; d < ND; ++d)
+          if (d != f) cnt *= ext[d];
+      }
+      const int64_t sv = stat_value(K, sum, cnt, mn, mx);
+      if (f == 0) s0 = sv;
+      if (group_lead) a.scalars[MODE == MODE_BLOCK ? bi : bi * ND + f] = sv;
+    }
+  }
+  if (MODE == MODE_GLOBAL) {
+    gacc.merge(tacc);
+    gcnt += tcnt;
+  }
+  if (group_lead) {
+    int64_t total = run;
+    if (MODE != MODE_GLOBAL) {
+      const int64_t d = (int64_t)d_origin - s0;
+      const bool o = bad_origin || d > (int64_t)(R - 1) || d < -(int64_t)(R - 1);
+      a.codes[bstart] = o ? (uint16_t)0 : (uint16_t)(d + R);
+      if (o) {
+        a.scratch[bstart] = v_origin;
+        total += 1;
+      }
+    }
+    a.counts[bi] = total;
+  }
+}
+
+template <int ND, int B, int VPL, int MODE, int K>
+__global__ void __launch_bounds__(FAST_WARPS * 32, 4) dq_compress_fast_kernel(FastArgs fa) {
+  using S = Shape<ND, B, VPL>;
+  using F = FastShape<ND, B, VPL>;
+  extern __shared__ __align__(128) unsigned char smem_fast[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  float* ring = reinterpret_cast<float*>(smem_fast + (size_t)wib * F::WARP_SMEM);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_fast + (size_t)wib * F::WARP_SMEM +
+                                               FAST_STAGES * F::PLANE_BYTES + F::PREV_BYTES);
+  const Geo& g = fa.c.g;
+
+  if (lane == 0) {
+    for (int s = 0; s < FAST_STAGES; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+
+  const uint32_t nwarps = gridDim.x * FAST_WARPS;
+  const uint32_t first = blockIdx.x * FAST_WARPS + wib;
+  Producer<ND, B, VPL> prod;
+  prod.start(g, fa.c.in, first);
+  for (int s = 0; s < FAST_STAGES; ++s) prod.issue(g, fa.c.in, ring, bars, lane, nwarps);
+  Consumer<ND, B, VPL> cons{0, 0u};
+  KAcc<K> gacc;
+  long long gcnt = 0;
+
+  for (uint32_t tile = first; tile < (uint32_t)g.ntiles; tile += nwarps) {
+    const TileXY tc = decode_tile(g, tile);
+    const bool interior = ((int64_t)(tc.wx + 1) * S::W <= g.D2) &&
+                          ((int64_t)(tc.by + 1) * S::BY <= g.D1);
+    if (interior)
+      fast_tile<ND, B, VPL, MODE, K, true>(fa, tile, tc, lane, ring, bars, prod, cons, nwarps,
+                                           gacc, gcnt);
+    else
+      fast_tile<ND, B, VPL, MODE, K, false>(fa, tile, tc, lane, ring, bars, prod, cons, nwarps,
+                                            gacc, gcnt);
+  }
+
+  if (MODE == MODE_GLOBAL) {
+    const CompressArgs& a = fa.c;
+    long long s = gacc.sum, c = gcnt;
+    int mn = gacc.mn, mx = gacc.mx;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      s += __shfl_xor_sync(FULL, s, o);
+      c += __shfl_xor_sync(FULL, c, o);
+      const int m1 = __shfl_xor_sync(FULL, mn, o);
+      const int m2 = __shfl_xor_sync(FULL, mx, o);
+      mn = m1 < mn ? m1 : mn;
+      mx = m2 > mx ? m2 : mx;
+    }
+    if (lane == 0 && c > 0) {
+      atomicAdd(a.gsum, (unsigned long long)s);
+      atomicAdd(a.gcount, (unsigned long long)c);
+      atomicMin(a.gmin, (long long)mn);
+      atomicMin(a.gnegmax, -(long long)mx);
+    }
+  }
+}
+
+}  // namespace vlz

@@ -43,6 +43,8 @@ struct DecompressArgs {
   int* status;
   long long* index;
   long long* n_sent_out;
+  const unsigned int* redo_count;  // tiles queued by the fast kernel
+  const long long* redo_list;
 };
 
 template <typename CT, int VPL>
@@ -250,7 +252,9 @@ __device__ __forceinline__ void decompress_tile(const DecompressArgs& a, int64_t
   }
 }
 
-template <int ND, int B, int VPL, typename CT>
+// LIST = true: only the tiles queued by dq_decompress_fast_kernel (edge tiles
+// and tiles that failed the int32 exactness check), in int64 as always.
+template <int ND, int B, int VPL, typename CT, bool LIST = false>
 __global__ void __launch_bounds__(128) dq_decompress_kernel(DecompressArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int PB = plane_smem_bytes<ND, B, VPL>();
@@ -259,9 +263,9 @@ __global__ void __launch_bounds__(128) dq_decompress_kernel(DecompressArgs a) {
   long long* wsm = reinterpret_cast<long long*>(smem_raw + (size_t)wib * PB);
   long long sent = 0;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t tile = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib; tile < a.g.ntiles;
-       tile += nwarps)
-    decompress_tile<ND, B, VPL, CT>(a, tile, lane, wsm, sent);
+  const int64_t ntodo = LIST ? (int64_t)*a.redo_count : a.g.ntiles;
+  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib; i < ntodo; i += nwarps)
+    decompress_tile<ND, B, VPL, CT>(a, LIST ? a.redo_list[i] : i, lane, wsm, sent);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) sent += __shfl_xor_sync(FULL, sent, o);
   if (lane == 0 && sent) atomicAdd(a.sentinels, (unsigned long long)sent);

@@ -1,25 +1,14 @@
-// k_compress_nd2.cu -- instantiations of the fused compress kernel for 2-D arrays.
-#include "launch.cuh"
+// k_compress_nd2.cu -- compress kernel instantiations for 2-D arrays.
+#include "launch_compress.cuh"
 
 namespace vlz {
 
-template <int B, int VPL>
-static cudaError_t run_b(int mode, const CompressArgs& a, cudaStream_t st) {
-  constexpr int smem = 4 * plane_smem_bytes<2, B, VPL>();
-  switch (mode) {
-    case MODE_ZERO: return launch_tiles(dq_compress_kernel<2, B, VPL, MODE_ZERO>, a.g.ntiles, smem, st, a);
-    case MODE_GLOBAL: return launch_tiles(dq_compress_kernel<2, B, VPL, MODE_GLOBAL>, a.g.ntiles, smem, st, a);
-    case MODE_BLOCK: return launch_tiles(dq_compress_kernel<2, B, VPL, MODE_BLOCK>, a.g.ntiles, smem, st, a);
-    default: return launch_tiles(dq_compress_kernel<2, B, VPL, MODE_EDGE>, a.g.ntiles, smem, st, a);
-  }
-}
-
 cudaError_t launch_compress_nd2(int B, int mode, const CompressArgs& a, cudaStream_t st) {
   switch (B) {
-    case 8: return run_b<8, 4>(mode, a, st);
-    case 16: return run_b<16, 4>(mode, a, st);
-    case 32: return run_b<32, 4>(mode, a, st);
-    case 64: return run_b<64, 4>(mode, a, st);
+    case 8: return run_compress_b<2, 8, 4>(mode, a, st);
+    case 16: return run_compress_b<2, 16, 2>(mode, a, st);
+    case 32: return run_compress_b<2, 32, 4>(mode, a, st);
+    case 64: return run_compress_b<2, 64, 4>(mode, a, st);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -1,11 +1,60 @@
-// k_decompress.cu -- instantiations of the fused reconstruction kernel.
+// k_decompress.cu -- reconstruction kernel instantiations and dispatch.
+//   fast shapes (3-D b=8/16, 2-D b=8/16), uint16 codes, aligned buffers:
+//       dq_decompress_fast_kernel (interior tiles, int32 with exactness check)
+//       + dq_decompress_kernel<LIST> (edge / flagged tiles, int64)
+//   everything else: dq_decompress_kernel (int64)
+#include "dq_decompress_fast.cuh"
 #include "launch.cuh"
 
 namespace vlz {
 
+template <int ND, int B>
+constexpr bool has_dfast() {
+  return (ND == 3 || ND == 2) && (B == 8 || B == 16);
+}
+
 template <int ND, int B, int VPL>
 static cudaError_t run_d(bool u32, const DecompressArgs& a, cudaStream_t st) {
   constexpr int smem = 4 * plane_smem_bytes<ND, B, VPL>();
+  if constexpr (has_dfast<ND, B>()) {
+    const bool aligned = !u32 && (a.g.D2 % 4 == 0) &&
+                         ((reinterpret_cast<uintptr_t>(a.codes) & 15) == 0) &&
+                         ((reinterpret_cast<uintptr_t>(a.out) & 15) == 0) &&
+                         a.redo_list != nullptr && a.g.ntiles < (1ll << 30) &&
+                         (a.q.twoeb < 1e300);
+    if (aligned) {
+      auto kern = dq_decompress_fast_kernel<ND, B, VPL>;
+      constexpr int fsmem = dfast_smem_bytes<ND, B, VPL>();
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem);
+      if (e != cudaSuccess) return e;
+      int per_sm = 0;
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, FAST_WARPS * 32, fsmem);
+      if (e != cudaSuccess) return e;
+      if (per_sm < 1) per_sm = 1;
+      int64_t grid = (int64_t)per_sm * num_sms();
+      const int64_t need = (a.g.ntiles + FAST_WARPS - 1) / FAST_WARPS;
+      if (grid > need) grid = need;
+      if (grid < 1) grid = 1;
+      DFastArgs fa{a, const_cast<unsigned int*>(a.redo_count), const_cast<long long*>(a.redo_list)};
+      const bool t = g_timing.load(std::memory_order_relaxed);
+      if (t) timing_mark(TK_DECOMPRESS, true, st);
+      kern<<<(unsigned)grid, FAST_WARPS * 32, fsmem, st>>>(fa);
+      if (t) timing_mark(TK_DECOMPRESS, false, st);
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+      e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+      auto redo = dq_decompress_kernel<ND, B, VPL, uint16_t, true>;
+      if (smem > 48 * 1024) {
+        e = cudaFuncSetAttribute(redo, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+      }
+      if (t) timing_mark(TK_REDO, true, st);
+      redo<<<(unsigned)num_sms() * 2, 128, smem, st>>>(a);
+      if (t) timing_mark(TK_REDO, false, st);
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+      return cudaGetLastError();
+    }
+  }
   if (u32) return launch_tiles(dq_decompress_kernel<ND, B, VPL, uint32_t>, a.g.ntiles, smem, st, a);
   return launch_tiles(dq_decompress_kernel<ND, B, VPL, uint16_t>, a.g.ntiles, smem, st, a);
 }
@@ -22,14 +71,14 @@ cudaError_t launch_decompress(int nd, int B, bool u32, const DecompressArgs& a, 
   } else if (nd == 2) {
     switch (B) {
       case 8: return run_d<2, 8, 4>(u32, a, st);
-      case 16: return run_d<2, 16, 4>(u32, a, st);
+      case 16: return run_d<2, 16, 2>(u32, a, st);
       case 32: return run_d<2, 32, 4>(u32, a, st);
       case 64: return run_d<2, 64, 4>(u32, a, st);
     }
   } else if (nd == 3) {
     switch (B) {
       case 8: return run_d<3, 8, 4>(u32, a, st);
-      case 16: return run_d<3, 16, 4>(u32, a, st);
+      case 16: return run_d<3, 16, 2>(u32, a, st);
       case 32: return run_d<3, 32, 4>(u32, a, st);
       case 64: return run_d<3, 64, 2>(u32, a, st);
     }

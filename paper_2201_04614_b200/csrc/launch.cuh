@@ -17,7 +17,7 @@ int num_sms();
 
 // optional per-kernel CUDA-event timing (vlz_timing / vlz_timing_collect)
 enum TimedKind { TK_INIT = 0, TK_COMPRESS = 1, TK_SCAN_C = 2, TK_SCAN_D = 3, TK_DECOMPRESS = 4,
-                 TK_MINMAX = 5, TK_COUNT = 6 };
+                 TK_MINMAX = 5, TK_REDO = 6, TK_COUNT = 8 };
 extern std::atomic<int> g_timing;
 void timing_mark(int kind, bool start, cudaStream_t st);
 
@@ -55,6 +55,7 @@ cudaError_t launch_decompress(int nd, int B, bool u32, const DecompressArgs& a, 
 inline int vpl_for(int nd, int B) {
   if (nd == 1 && B == 256) return 8;
   if (nd == 3 && B == 64) return 2;
+  if (nd >= 2 && B == 16) return 2;
   return 4;
 }
 

@@ -1,0 +1,82 @@
+// launch_compress.cuh -- per-shape launch of the compress kernels.
+//   fast shapes (3-D b=8/16, 2-D b=8/16) with 16-byte aligned rows:
+//       dq_compress_fast_kernel  +  int64 redo of listed tiles
+//   everything else: dq_compress_kernel (generic, uint32/int64 per tile)
+#pragma once
+
+#include <cstdint>
+
+#include "dq_compress_fast.cuh"
+#include "launch.cuh"
+
+namespace vlz {
+
+template <int ND, int B>
+constexpr bool has_fast() {
+  return (ND == 3 || ND == 2) && (B == 8 || B == 16);
+}
+
+template <int ND, int B, int VPL, int MODE, int K>
+cudaError_t run_compress_shape(const CompressArgs& a, cudaStream_t st) {
+  constexpr int smem = 4 * plane_smem_bytes<ND, B, VPL>();
+  if constexpr (has_fast<ND, B>()) {
+    const bool aligned = (a.g.D2 % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.in) & 15) == 0);
+    if (aligned && a.redo_list != nullptr && a.g.ntiles < (1ll << 30)) {
+      auto kern = dq_compress_fast_kernel<ND, B, VPL, MODE, K>;
+      constexpr int fsmem = fast_smem_bytes<ND, B, VPL>();
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem);
+      if (e != cudaSuccess) return e;
+      int per_sm = 0;
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, FAST_WARPS * 32, fsmem);
+      if (e != cudaSuccess) return e;
+      if (per_sm < 1) per_sm = 1;
+      int64_t grid = (int64_t)per_sm * num_sms();
+      const int64_t need = (a.g.ntiles + FAST_WARPS - 1) / FAST_WARPS;
+      if (grid > need) grid = need;
+      if (grid < 1) grid = 1;
+      FastArgs fa{a, const_cast<unsigned int*>(a.redo_count), const_cast<long long*>(a.redo_list)};
+      const bool t = g_timing.load(std::memory_order_relaxed);
+      if (t) timing_mark(TK_COMPRESS, true, st);
+      kern<<<(unsigned)grid, FAST_WARPS * 32, fsmem, st>>>(fa);
+      if (t) timing_mark(TK_COMPRESS, false, st);
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+      e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+      // int64 redo of tiles whose |d| reached 2^24 (usually none: exits at once)
+      auto redo = dq_compress_kernel<ND, B, VPL, MODE, true>;
+      if (smem > 48 * 1024) {
+        e = cudaFuncSetAttribute(redo, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+      }
+      if (t) timing_mark(TK_REDO, true, st);
+      redo<<<(unsigned)num_sms(), 128, smem, st>>>(a);
+      if (t) timing_mark(TK_REDO, false, st);
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+      return cudaGetLastError();
+    }
+  }
+  return launch_tiles(dq_compress_kernel<ND, B, VPL, MODE, false>, a.g.ntiles, smem, st, a);
+}
+
+template <int ND, int B, int VPL, int MODE>
+cudaError_t run_compress_k(int kind, const CompressArgs& a, cudaStream_t st) {
+  if constexpr (has_fast<ND, B>()) {
+    if (kind == 1) return run_compress_shape<ND, B, VPL, MODE, 1>(a, st);
+    if (kind == 2) return run_compress_shape<ND, B, VPL, MODE, 2>(a, st);
+    return run_compress_shape<ND, B, VPL, MODE, 3>(a, st);
+  } else {
+    return run_compress_shape<ND, B, VPL, MODE, 3>(a, st);
+  }
+}
+
+template <int ND, int B, int VPL>
+cudaError_t run_compress_b(int mode, const CompressArgs& a, cudaStream_t st) {
+  switch (mode) {
+    case MODE_ZERO: return run_compress_shape<ND, B, VPL, MODE_ZERO, 0>(a, st);
+    case MODE_GLOBAL: return run_compress_k<ND, B, VPL, MODE_GLOBAL>(a.q.kind, a, st);
+    case MODE_BLOCK: return run_compress_k<ND, B, VPL, MODE_BLOCK>(a.q.kind, a, st);
+    default: return run_compress_k<ND, B, VPL, MODE_EDGE>(a.q.kind, a, st);
+  }
+}
+
+}  // namespace vlz

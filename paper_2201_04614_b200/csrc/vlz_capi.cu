@@ -100,6 +100,8 @@ bool make_geo(const vlz_geom* gg, Geo& g) {
   g.ntiles = g.P0 * g.P1 * g.NW;
   g.nblocks = g.P0 * g.P1 * g.P2;
   g.N = D[0] * D[1] * D[2];
+  g.divNW.init((uint32_t)(g.NW < 0xffffffffll ? g.NW : 1));
+  g.divP1.init((uint32_t)(g.P1 < 0xffffffffll ? g.P1 : 1));
   return true;
 }
 
@@ -121,9 +123,11 @@ bool valid_params(const vlz_params* p) {
 struct WS {
   unsigned int* ticket;      // scan chunk ticket
   unsigned int* done;        // finished-CTA counter
+  unsigned int* redo_count;  // tiles queued for the int64 redo
   long long* stats;          // sum, count, min, neg_max (single-GPU compress)
   long long* aux;            // 8 spare words
   unsigned long long* lb;    // look-back words, one per scan chunk
+  long long* redo_list;      // ntiles
   int64_t* offsets;          // nblocks
   float* scratch;            // N
   size_t bytes;
@@ -135,12 +139,15 @@ WS carve(const Geo& g, void* base) {
   size_t off = 0;
   w.ticket = reinterpret_cast<unsigned int*>(p + off);
   w.done = reinterpret_cast<unsigned int*>(p + off + 8);
+  w.redo_count = reinterpret_cast<unsigned int*>(p + off + 16);
   w.stats = reinterpret_cast<long long*>(p + off + 64);
   w.aux = reinterpret_cast<long long*>(p + off + 128);
   off += 256;
   const int64_t nchunks = (g.nblocks + SCAN_CH - 1) / SCAN_CH;
   w.lb = reinterpret_cast<unsigned long long*>(p + off);
   off += align256((size_t)nchunks * 8);
+  w.redo_list = reinterpret_cast<long long*>(p + off);
+  off += align256((size_t)g.ntiles * 8);
   w.offsets = reinterpret_cast<int64_t*>(p + off);
   off += align256((size_t)g.nblocks * 8);
   w.scratch = reinterpret_cast<float*>(p + off);
@@ -167,6 +174,7 @@ __global__ void init_kernel(vlz_result* res, unsigned int* ticket, unsigned int*
     }
     *ticket = 0;
     *done = 0;
+    ticket[4] = 0;  // redo_count (workspace offset 16)
     if (stats) {
       stats[0] = 0;
       stats[1] = 0;
@@ -214,6 +222,12 @@ QP make_qp(const vlz_params* p) {
   q.twoeb = 2.0 * p->eb;
   q.radius = p->radius;
   q.kind = p->pad_kind;
+  // float32 fast path only where 1/(2eb) is a normal float with margin
+  const double inv = 1.0 / q.twoeb;
+  const bool fast_ok = q.twoeb > 0.0 && inv > 0x1p-100 && inv < 0x1p100;
+  q.inv32 = fast_ok ? (float)inv : 0.0f;
+  q.lim0 = fast_ok ? (float)(0.5 - 0x1p-22) : -1.0f;
+  q.kq = (float)0x1p-21;
   return q;
 }
 
@@ -335,6 +349,8 @@ static int compress_begin_impl(const float* d_in, const vlz_geom* gg, const vlz_
   a.gcount = reinterpret_cast<unsigned long long*>(stats ? stats + 1 : nullptr);
   a.gmin = stats ? stats + 2 : nullptr;
   a.gnegmax = stats ? stats + 3 : nullptr;
+  a.redo_count = w.redo_count;
+  a.redo_list = w.redo_list;
   const int b = gg->block_edge;
   if (gg->nd == 1) e = launch_compress_nd1(b, mode, a, st);
   else if (gg->nd == 2) e = launch_compress_nd2(b, mode, a, st);
@@ -460,6 +476,8 @@ static int decompress_impl(const void* d_codes, bool u32, const float* d_outlier
   a.status = &d_result->status;
   a.index = reinterpret_cast<long long*>(&d_result->index);
   a.n_sent_out = reinterpret_cast<long long*>(&d_result->n_outliers);
+  a.redo_count = w.redo_count;
+  a.redo_list = w.redo_list;
   return to_rc(launch_decompress(gg->nd, b, u32, a, st));
 }
 

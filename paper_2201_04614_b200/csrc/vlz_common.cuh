@@ -19,6 +19,30 @@ namespace vlz {
 
 constexpr unsigned FULL = 0xffffffffu;
 
+// Division of 32-bit unsigned values by a launch-invariant divisor d >= 1
+// (Granlund-Montgomery with the add-shift fix-up; exact for every x < 2^32).
+struct FastDiv {
+  uint32_t d, m, s;
+  __host__ void init(uint32_t div) {
+    d = div;
+    if (div <= 1) {
+      d = 1;
+      m = 0;
+      s = 0;
+      return;
+    }
+    uint32_t l = 0;
+    while ((1ull << l) < div) ++l;
+    s = l;
+    m = (uint32_t)(((1ull << 32) * ((1ull << l) - div)) / div + 1);
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t x) const {
+    if (d == 1) return x;
+    const uint32_t t = __umulhi(m, x);
+    return (t + ((x - t) >> 1)) >> (s - 1);
+  }
+};
+
 // Padded 3-D view of a 1/2/3-D array: dims (D0, D1, D2) with leading 1s, so a
 // 1-D array is (1, 1, N) and a 2-D array (1, Y, X).  Block extents per padded
 // dim are (BZ, BY, BX) = (B if nd == 3 else 1, B if nd >= 2 else 1, B).
@@ -29,6 +53,7 @@ struct Geo {
   int64_t ntiles;      // P0 * P1 * NW
   int64_t nblocks;
   int64_t N;
+  FastDiv divNW, divP1;  // 32-bit tile decode (valid when ntiles < 2^31)
 };
 
 struct QP {
@@ -36,7 +61,32 @@ struct QP {
   double twoeb;  // 2.0 * eb (exact)
   int radius;
   int kind;      // VLZ_PAD_* (min / max / mean used by the statistics)
+  // float32 fast path (quant_fast); lim0 < 0 disables it
+  float inv32;   // fl32(1 / (2 eb))
+  float lim0;    // 0.5 - 2^-22
+  float kq;      // 2^-21
 };
+
+// Fast exact prequantization ("fast path proof").
+// q = fl32(v * fl32(1/(2eb))) is within |q| * 2^-22 of fl64(v / (2eb)); the
+// magic-number add rounds q to nearest (n) and e = q - n is exact.  When the
+// distance of q to the rounding boundary, 0.5 - |e|, exceeds
+// |q| * 2^-21 + 2^-22, then (a) round_half_away(fl64(v/(2eb))) == n (no
+// boundary lies between the two quotients, and no tie is possible) and
+// (b) the float32-narrowed reconstruction of n is within eb of v (the f32
+// rounding of n*2eb moves it by at most |q| * 2^-23 * 2eb).  Otherwise the
+// caller re-evaluates the element with quant_exact.  |q| >= 2^21, NaN and
+// Inf always fail the test.
+__device__ __forceinline__ int quant_fast(float v, const QP& q, bool& ok) {
+  const float qq = __fmul_rn(v, q.inv32);
+  const float r = __fadd_rn(qq, 12582912.0f);  // 1.5 * 2^23: RN to an integer
+  const int n = __float_as_int(r) - 0x4B400000;
+  const float e = __fsub_rn(qq, __fsub_rn(r, 12582912.0f));
+  const float lim = __fmaf_rn(fabsf(qq), -q.kq, q.lim0);
+  ok = fabsf(e) < lim;
+  return n;
+}
+
 
 // canonical start of a block's codes: number of in-bounds elements of all
 // earlier blocks in row-major block order (vector.py:193-202 ordering)
