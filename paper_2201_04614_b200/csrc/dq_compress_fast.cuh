@@ -21,6 +21,8 @@
 // identical to dq_compress.cuh.
 #pragma once
 
+#include <cuda.h>
+
 #include "dq_compress.cuh"
 #include "tma.cuh"
 
@@ -36,7 +38,7 @@ struct FastShape {
   static constexpr int PLANE_BYTES = PLANE_FLOATS * 4;
   // ring of input planes + the previous plane's Dy Dx d (int32, 3-D only)
   static constexpr int PREV_BYTES = (ND == 3) ? PLANE_BYTES : 0;
-  static constexpr int WARP_SMEM = FAST_STAGES * PLANE_BYTES + PREV_BYTES + 64;
+  static constexpr int WARP_SMEM = (FAST_STAGES * PLANE_BYTES + PREV_BYTES + 64 + 127) / 128 * 128;
 };
 
 template <int ND, int B, int VPL>
@@ -45,6 +47,7 @@ __host__ __device__ constexpr int fast_smem_bytes() {
 }
 
 struct FastArgs {
+  CUtensorMap tmap;  // input viewed as (D2, D1, D0) uint32, box (W, BY, 1)
   CompressArgs c;
   unsigned int* redo_count;
   long long* redo_list;
@@ -63,49 +66,44 @@ __device__ __forceinline__ TileXY decode_tile(const Geo& g, uint32_t tile) {
   return t;
 }
 
-// producer side of the per-warp plane ring
+// producer side of the per-warp plane ring: one TMA tensor load per plane
 template <int ND, int B, int VPL>
 struct Producer {
   using S = Shape<ND, B, VPL>;
-  uint32_t tile;       // current tile (>= ntiles: done)
-  int zl, ez, ey;
-  const float* src;    // first row of the current plane
-  uint32_t row_bytes;
+  uint32_t tile;  // current tile (>= ntiles: done)
+  int zl, ez;
+  int x0, y0, z0;
   int stage;
 
-  __device__ __forceinline__ void start(const Geo& g, const float* in, uint32_t t) {
+  __device__ __forceinline__ void start(const Geo& g, uint32_t t) {
     tile = t;
     zl = 0;
     stage = 0;
-    setup(g, in);
+    setup(g);
   }
-  __device__ __forceinline__ void setup(const Geo& g, const float* in) {
+  __device__ __forceinline__ void setup(const Geo& g) {
     if (tile >= (uint32_t)g.ntiles) return;
     const TileXY c = decode_tile(g, tile);
-    const int64_t z0 = (int64_t)c.bz * S::BZ, y0 = (int64_t)c.by * S::BY;
-    const int64_t x0 = (int64_t)c.wx * S::W;
+    z0 = (int)c.bz * S::BZ;
+    y0 = (int)c.by * S::BY;
+    x0 = (int)c.wx * S::W;
     ez = (int)imin64(S::BZ, g.D0 - z0);
-    ey = (int)imin64(S::BY, g.D1 - y0);
-    row_bytes = (uint32_t)imin64(S::W, g.D2 - x0) * 4u;
-    src = in + (z0 * g.D1 + y0) * g.D2 + x0;
   }
   // issue the current plane into `stage`, then advance (all lanes call)
-  __device__ __forceinline__ void issue(const Geo& g, const float* in, float* ring,
+  __device__ __forceinline__ void issue(const Geo& g, const CUtensorMap* tmap, float* ring,
                                         uint64_t* bars, int lane, uint32_t nwarps) {
     using F = FastShape<ND, B, VPL>;
     if (tile >= (uint32_t)g.ntiles) return;
-    float* buf = ring + stage * F::PLANE_FLOATS;
-    uint64_t* bar = &bars[stage];
-    if (lane == 0) mbar_arrive_expect_tx(bar, row_bytes * (uint32_t)ey);
-    __syncwarp();
-    if (lane < ey) bulk_g2s(buf + lane * S::W, src + (int64_t)lane * g.D2, row_bytes, bar);
+    if (lane == 0) {
+      uint64_t* bar = &bars[stage];
+      mbar_arrive_expect_tx(bar, (uint32_t)F::PLANE_BYTES);
+      tma_load_3d(ring + stage * F::PLANE_FLOATS, tmap, x0, y0, z0 + zl, bar);
+    }
     if (++stage == FAST_STAGES) stage = 0;
-    if (++zl < ez) {
-      src += g.D1 * g.D2;
-    } else {
+    if (++zl >= ez) {
       zl = 0;
       tile += nwarps;
-      setup(g, in);
+      setup(g);
     }
   }
 };
@@ -379,7 +377,7 @@ __device__ __forceinline__ void fast_tile(const FastArgs& fa, uint32_t tile, con
     // release the slot and refill it FAST_STAGES planes ahead
     __syncwarp();
     fence_proxy_async_smem();
-    prod.issue(g, a.in, ring, bars, lane, nwarps);
+    prod.issue(g, &fa.tmap, ring, bars, lane, nwarps);
     cons.advance();
   }
 
@@ -435,7 +433,8 @@ __device__ __forceinline__ void fast_tile(const FastArgs& fa, uint32_t tile, con
 }
 
 template <int ND, int B, int VPL, int MODE, int K>
-__global__ void __launch_bounds__(FAST_WARPS * 32, 4) dq_compress_fast_kernel(FastArgs fa) {
+__global__ void __launch_bounds__(FAST_WARPS * 32, 4)
+    dq_compress_fast_kernel(const __grid_constant__ FastArgs fa) {
   using S = Shape<ND, B, VPL>;
   using F = FastShape<ND, B, VPL>;
   extern __shared__ __align__(128) unsigned char smem_fast[];
@@ -454,9 +453,10 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, 4) dq_compress_fast_kernel(Fa
 
   const uint32_t nwarps = gridDim.x * FAST_WARPS;
   const uint32_t first = blockIdx.x * FAST_WARPS + wib;
+  if (threadIdx.x == 0) prefetch_tmap(&fa.tmap);
   Producer<ND, B, VPL> prod;
-  prod.start(g, fa.c.in, first);
-  for (int s = 0; s < FAST_STAGES; ++s) prod.issue(g, fa.c.in, ring, bars, lane, nwarps);
+  prod.start(g, first);
+  for (int s = 0; s < FAST_STAGES; ++s) prod.issue(g, &fa.tmap, ring, bars, lane, nwarps);
   Consumer<ND, B, VPL> cons{0, 0u};
   KAcc<K> gacc;
   long long gcnt = 0;

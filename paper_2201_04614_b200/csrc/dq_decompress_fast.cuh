@@ -5,17 +5,17 @@
 // E = G + E(prev plane), d = E + s0, out = float32(fl64(2 d eb))), specialised
 // for the throughput shapes (3-D b=8/16, 2-D b=8/16) and interior tiles:
 //
-//  * each plane of a tile is W/BX contiguous block slices of BY*BX uint16
-//    codes; they stream into a per-warp shared ring with TMA bulk copies
-//    (one cp.async.bulk per block slice, slices padded so that the lanes'
-//    vector LDS hit distinct banks), FAST_STAGES planes ahead;
-//  * arithmetic is wrapping int32.  It is exact whenever every reconstructed
-//    |E| and every sentinel |d - s0| stays below 2^28 and |s0| < 2^28: by
-//    induction over the traversal order each true value is then a sum of
-//    7 earlier values (< 7 * 2^28) plus a code (< 2^15), i.e. it lies in
-//    (-2^31, 2^31) where congruence mod 2^32 is equality.  The kernel checks
-//    exactly that and hands any tile that fails it -- and every edge tile --
-//    to the int64 kernel (dq_decompress_kernel<..., LIST=true>);
+//  * each lane streams its own VPL codes of every row of a plane into a
+//    per-warp shared ring with cp.async (LDGSTS), FAST_STAGES planes ahead
+//    and across tile boundaries; the [row][lane] layout makes the later
+//    vector LDS conflict-free and needs no cross-lane barrier;
+//  * arithmetic is wrapping int32.  It is exact whenever |s0| < 2^27 and every
+//    computed |d| < 2^27: by induction over the traversal order, the true
+//    E = d - s0 of each element is a signed sum of 7 earlier exact values
+//    (each < 2^28) plus a code (< 2^15), so it lies in (-2^31, 2^31) where
+//    congruence mod 2^32 is equality.  The kernel checks exactly that and
+//    hands any tile that fails it -- and every edge tile -- to the int64
+//    kernel (dq_decompress_kernel<..., LIST=true>);
 //  * output rows leave with 16-byte stores straight from registers.
 #pragma once
 
@@ -27,15 +27,14 @@ namespace vlz {
 template <int ND, int B, int VPL>
 struct DFastShape {
   using S = Shape<ND, B, VPL>;
-  static constexpr int NBLK = S::W / S::BX;                 // blocks per window
-  static constexpr int SLICE_CODES = S::BY * S::BX;          // codes per block plane
-  static constexpr int SLICE_BYTES = SLICE_CODES * 2;
-  // pad each slice so consecutive blocks start 4 (B=8) / 8 (B>=16) banks apart
-  static constexpr int PAD_BYTES = (S::BX == 8) ? 16 : 32;
-  static constexpr int SLOT_BYTES = SLICE_BYTES + PAD_BYTES;
-  static constexpr int STAGE_BYTES = NBLK * SLOT_BYTES;
+  static constexpr int NBLK = S::W / S::BX;         // blocks per window
+  static constexpr int SLICE_CODES = S::BY * S::BX;  // codes per block plane
+  // stage layout [row][lane] x VPL codes: every lane copies (cp.async) and
+  // later reads its own VPL codes of each row -- conflict-free, no barrier
+  static constexpr int LANE_BYTES = VPL * 2;
+  static constexpr int STAGE_BYTES = S::BY * 32 * LANE_BYTES;
   static constexpr int PREV_BYTES = (ND == 3) ? S::BY * S::W * 4 : 0;
-  static constexpr int WARP_SMEM = FAST_STAGES * STAGE_BYTES + PREV_BYTES + 64;
+  static constexpr int WARP_SMEM = FAST_STAGES * STAGE_BYTES + PREV_BYTES;
 };
 
 template <int ND, int B, int VPL>
@@ -55,26 +54,30 @@ __device__ __forceinline__ bool tile_interior(const Geo& g, const TileXY& c) {
   return ((int64_t)(c.wx + 1) * S::W <= g.D2) && ((int64_t)(c.by + 1) * S::BY <= g.D1);
 }
 
-// producer of code planes (interior tiles only; others are skipped)
+// per-lane producer of code planes (interior tiles only; others are skipped).
+// Every issue() commits exactly one cp.async group (possibly empty), so
+// cp.async.wait_group<FAST_STAGES-1> always retires the plane being consumed.
 template <int ND, int B, int VPL>
 struct DProducer {
   using S = Shape<ND, B, VPL>;
   using F = DFastShape<ND, B, VPL>;
   uint32_t tile;
   int zl, ez;
-  const uint16_t* src;  // block 0's slice of the current plane
-  int64_t plane_stride; // codes between consecutive planes of one block
+  const uint16_t* src;  // this lane's codes in plane 0, row 0 of the current tile
   int stage;
 
-  __device__ __forceinline__ void seek(const Geo& g, const uint16_t* codes, uint32_t nwarps) {
+  __device__ __forceinline__ void seek(const Geo& g, const uint16_t* codes, uint32_t nwarps,
+                                       int lane) {
     while (tile < (uint32_t)g.ntiles) {
       const TileXY c = decode_tile(g, tile);
       if (tile_interior<ND, B, VPL>(g, c)) {
         const int64_t z0 = (int64_t)c.bz * S::BZ;
         ez = (int)imin64(S::BZ, g.D0 - z0);
+        const int blk = (lane * VPL) / S::BX;
         const int64_t bx0 = (int64_t)c.wx * F::NBLK;
-        src = codes + block_start(g, c.bz, c.by, bx0, S::BZ, S::BY, S::BX, ez, S::BY);
-        plane_stride = F::SLICE_CODES;
+        // consecutive full blocks of the window: ez * BY * BX codes each
+        src = codes + block_start(g, c.bz, c.by, bx0, S::BZ, S::BY, S::BX, ez, S::BY) +
+              (int64_t)blk * ez * F::SLICE_CODES + (lane * VPL) % S::BX;
         zl = 0;
         return;
       }
@@ -82,35 +85,32 @@ struct DProducer {
     }
   }
   __device__ __forceinline__ void start(const Geo& g, const uint16_t* codes, uint32_t t,
-                                        uint32_t nwarps) {
+                                        uint32_t nwarps, int lane) {
     tile = t;
     stage = 0;
-    seek(g, codes, nwarps);
+    seek(g, codes, nwarps, lane);
   }
   __device__ __forceinline__ void issue(const Geo& g, const uint16_t* codes,
-                                        unsigned char* ring, uint64_t* bars, int lane,
-                                        uint32_t nwarps) {
-    if (tile >= (uint32_t)g.ntiles) return;
-    unsigned char* buf = ring + stage * F::STAGE_BYTES;
-    uint64_t* bar = &bars[stage];
-    if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)(F::NBLK * F::SLICE_BYTES));
-    __syncwarp();
-    // block k of the window: its whole (full) block holds ez*BY*BX codes
-    if (lane < F::NBLK)
-      bulk_g2s(buf + lane * F::SLOT_BYTES,
-               src + (int64_t)lane * ez * F::SLICE_CODES + (int64_t)zl * plane_stride,
-               (uint32_t)F::SLICE_BYTES, bar);
-    if (++stage == FAST_STAGES) stage = 0;
-    if (++zl >= ez) {
-      tile += nwarps;
-      seek(g, codes, nwarps);
+                                        unsigned char* ring, uint32_t nwarps, int lane) {
+    if (tile < (uint32_t)g.ntiles) {
+      unsigned char* dst = ring + stage * F::STAGE_BYTES + lane * F::LANE_BYTES;
+      const uint16_t* s = src + (int64_t)zl * F::SLICE_CODES;
+#pragma unroll
+      for (int yl = 0; yl < S::BY; ++yl)
+        cp_async<F::LANE_BYTES>(dst + yl * 32 * F::LANE_BYTES, s + yl * S::BX);
+      if (++zl >= ez) {
+        tile += nwarps;
+        seek(g, codes, nwarps, lane);
+      }
     }
+    cp_async_commit();
+    if (++stage == FAST_STAGES) stage = 0;
   }
 };
 
 template <int ND, int B, int VPL>
 __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, const TileXY& tc,
-                                           int lane, unsigned char* ring, uint64_t* bars,
+                                           int lane, unsigned char* ring,
                                            DProducer<ND, B, VPL>& prod,
                                            Consumer<ND, B, VPL>& cons, uint32_t nwarps,
                                            long long& sent_acc) {
@@ -137,43 +137,50 @@ __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, c
   if (a.mode == MODE_GLOBAL) s064 = a.scalars[0];
   else if (a.mode == MODE_BLOCK) s064 = a.scalars[bi];
   else if (a.mode == MODE_EDGE) s064 = a.scalars[bi * a.nd];
-  wide |= (s064 >= (1ll << 28)) || (s064 <= -(1ll << 28));
+  wide |= (s064 >= (1ll << 27)) || (s064 <= -(1ll << 27));
   s0 = (int)s064;
   const long long off = a.offsets[bi];
   const long long avail = imax64(0, imin64(a.counts[bi], a.n_outliers - off));
 
+  // The outermost prefix state is primed with s0 (3-D: the previous-plane
+  // state starts at s0; 1-D/2-D: the previous-row state does), so d = E + s0
+  // comes out of the recurrence directly and a sentinel resets the x-scan to
+  // d_s - E'(prev plane) - G(prev row) with no s0 term.
   int* const pplane = reinterpret_cast<int*>(ring + FAST_STAGES * F::STAGE_BYTES) + lane * VPL;
   if (ND == 3) {
 #pragma unroll 1
     for (int yl = 0; yl < BY; ++yl) {
-      if (VPL == 4) *reinterpret_cast<int4*>(pplane + yl * W) = make_int4(0, 0, 0, 0);
-      else *reinterpret_cast<int2*>(pplane + yl * W) = make_int2(0, 0);
+      if (VPL == 4) *reinterpret_cast<int4*>(pplane + yl * W) = make_int4(s0, s0, s0, s0);
+      else *reinterpret_cast<int2*>(pplane + yl * W) = make_int2(s0, s0);
     }
   }
   int run = 0;
   bool badcode = false;
-  unsigned emag = 0;  // OR of (E + 2^28): stays < 2^29 iff every |E| < 2^28
+  unsigned dmag = 0;  // OR of (d + 2^27): stays < 2^28 iff every |d| < 2^27
   float* orow = a.out + (z0 * g.D1 + y0) * g.D2 + xl0;
+  const unsigned char* const slot0 = ring + lane * F::LANE_BYTES;
 
   for (int zl = 0; zl < ez; ++zl) {
-    const unsigned char* slot = ring + cons.stage * F::STAGE_BYTES + blk * F::SLOT_BYTES + xin * 2;
-    mbar_wait(&bars[cons.stage], cons.parity);
+    const unsigned char* slot = slot0 + cons.stage * F::STAGE_BYTES;
+    cp_async_wait<FAST_STAGES - 1>();
     int grow[VPL];
 #pragma unroll
-    for (int j = 0; j < VPL; ++j) grow[j] = 0;
+    for (int j = 0; j < VPL; ++j) grow[j] = (ND == 3) ? 0 : s0;
+    int* pp = pplane;
+    float* dst = orow;
 #pragma unroll 1
     for (int yl = 0; yl < BY; ++yl) {
       unsigned c[VPL];
       if (VPL == 4) {
-        const uint2 pk = *reinterpret_cast<const uint2*>(slot + yl * BX * 2);
+        const uint2 pk = *reinterpret_cast<const uint2*>(slot);
         c[0] = pk.x & 0xffffu; c[1 % VPL] = pk.x >> 16;
         c[2 % VPL] = pk.y & 0xffffu; c[3 % VPL] = pk.y >> 16;
       } else {
-        const unsigned pk = *reinterpret_cast<const unsigned*>(slot + yl * BX * 2);
+        const unsigned pk = *reinterpret_cast<const unsigned*>(slot);
         c[0] = pk & 0xffffu; c[1 % VPL] = pk >> 16;
       }
+      slot += 32 * F::LANE_BYTES;
       int ep[VPL];
-      int* pp = pplane + yl * W;
       if (ND == 3) {
         if (VPL == 4) {
           const int4 p4 = *reinterpret_cast<const int4*>(pp);
@@ -186,31 +193,40 @@ __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, c
 #pragma unroll
         for (int j = 0; j < VPL; ++j) ep[j] = 0;
       }
-      bool anysent = false, anybig = false;
+      bool anysent = false;
+      unsigned cmax = c[0];
 #pragma unroll
       for (int j = 0; j < VPL; ++j) {
         anysent = anysent || (c[j] == 0u);
-        anybig = anybig || (c[j] >= (unsigned)(2 * R));
+        cmax = c[j] > cmax ? c[j] : cmax;
       }
-      badcode |= anybig;
-      // in-lane inclusive scan of delta (no resets on the fast path)
+      badcode |= cmax >= (unsigned)(2 * R);
       int h[VPL];
-      h[0] = (int)c[0] - R;
-#pragma unroll
-      for (int j = 1; j < VPL; ++j) h[j] = h[j - 1] + ((int)c[j] - R);
-      bool reset_any = false;
-      unsigned before = (1u << VPL) - 1u;
       unsigned smask = 0;
       float vs[VPL];
-      if (__any_sync(FULL, anysent)) {
-        // rare: sentinels reset the scan to (d - s0) - E(prev plane) - G(prev row)
+      if (!__any_sync(FULL, anysent)) {
+        // common path: plain prefix of delta within the block's lanes
+        h[0] = (int)c[0] - R;
+#pragma unroll
+        for (int j = 1; j < VPL; ++j) h[j] = h[j - 1] + ((int)c[j] - R);
+        int inc = h[VPL - 1];
+#pragma unroll
+        for (int o = 1; o < LPB; o <<= 1) {
+          const int u = __shfl_up_sync(FULL, inc, o);
+          if (gl >= o) inc += u;
+        }
+        const int pv = inc - h[VPL - 1];  // exclusive carry from earlier lanes
+#pragma unroll
+        for (int j = 0; j < VPL; ++j) h[j] += pv;
+      } else {
+        // rare: sentinels reset the scan to d_s - E'(prev plane) - G(prev row)
 #pragma unroll
         for (int j = 0; j < VPL; ++j) smask |= (c[j] == 0u) ? (1u << j) : 0u;
         int tot;
         const int excl = group_excl_scan<LPB>(__popc(smask), lane, tot);
         int k = run + excl;
         int acc = 0;
-        before = 0;
+        unsigned before = 0;
         bool reset = false;
 #pragma unroll
         for (int j = 0; j < VPL; ++j) {
@@ -218,8 +234,8 @@ __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, c
           if ((smask >> j) & 1u) {
             if (k < avail) vs[j] = a.outliers[off + k];
             ++k;
-            const long long ds = quant_value(vs[j], a.q.twoeb) - s064;
-            wide |= (ds >= (1ll << 28)) || (ds <= -(1ll << 28));
+            const long long ds = quant_value(vs[j], a.q.twoeb);
+            wide |= (ds >= (1ll << 27)) || (ds <= -(1ll << 27));
             acc = (int)ds - ep[j] - grow[j];
             reset = true;
           } else {
@@ -228,33 +244,33 @@ __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, c
           if (!reset) before |= 1u << j;
           h[j] = acc;
         }
-        reset_any = reset;
         run += tot;
-      }
-      // carry across the block's lanes: segmented (flag, value) scan
-      int cv = h[VPL - 1];
-      bool cf = reset_any;
+        int cv = h[VPL - 1];
+        bool cf = reset;
 #pragma unroll
-      for (int o = 1; o < LPB; o <<= 1) {
-        const int uv = __shfl_up_sync(FULL, cv, o);
-        const bool uf = __shfl_up_sync(FULL, cf, o);
-        if (gl >= o && !cf) {
-          cv += uv;
-          cf = uf;
+        for (int o = 1; o < LPB; o <<= 1) {
+          const int uv = __shfl_up_sync(FULL, cv, o);
+          const bool uf = __shfl_up_sync(FULL, cf, o);
+          if (gl >= o && !cf) {
+            cv += uv;
+            cf = uf;
+          }
         }
+        int pv = __shfl_up_sync(FULL, cv, 1);
+        if (gl == 0) pv = 0;
+#pragma unroll
+        for (int j = 0; j < VPL; ++j)
+          if ((before >> j) & 1u) h[j] += pv;
       }
-      int pv = __shfl_up_sync(FULL, cv, 1);
-      if (gl == 0) pv = 0;
       float o[VPL];
-      int ev[VPL];
+      int dv[VPL];
 #pragma unroll
       for (int j = 0; j < VPL; ++j) {
-        const int hv = ((before >> j) & 1u) ? h[j] + pv : h[j];
-        const int gv = hv + grow[j];
+        const int gv = h[j] + grow[j];
         grow[j] = gv;
-        ev[j] = gv + ep[j];
-        emag |= (unsigned)(ev[j] + (1 << 28));
-        o[j] = __double2float_rn(__dmul_rn((double)(ev[j] + s0), a.q.twoeb));
+        dv[j] = gv + ep[j];  // = d (primed state)
+        dmag |= (unsigned)(dv[j] + (1 << 27));
+        o[j] = __double2float_rn(__dmul_rn((double)dv[j], a.q.twoeb));
       }
       if (smask) {
 #pragma unroll
@@ -262,20 +278,19 @@ __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, c
           if ((smask >> j) & 1u) o[j] = vs[j];
       }
       if (ND == 3) {
-        if (VPL == 4) *reinterpret_cast<int4*>(pp) = make_int4(ev[0], ev[1 % VPL], ev[2 % VPL], ev[3 % VPL]);
-        else *reinterpret_cast<int2*>(pp) = make_int2(ev[0], ev[1 % VPL]);
+        if (VPL == 4) *reinterpret_cast<int4*>(pp) = make_int4(dv[0], dv[1 % VPL], dv[2 % VPL], dv[3 % VPL]);
+        else *reinterpret_cast<int2*>(pp) = make_int2(dv[0], dv[1 % VPL]);
       }
-      float* dst = orow + yl * g.D2;
+      pp += W;
       if (VPL == 4) *reinterpret_cast<float4*>(dst) = make_float4(o[0], o[1 % VPL], o[2 % VPL], o[3 % VPL]);
       else *reinterpret_cast<float2*>(dst) = make_float2(o[0], o[1 % VPL]);
+      dst += g.D2;
     }
     orow += g.D1 * g.D2;
-    __syncwarp();
-    fence_proxy_async_smem();
-    prod.issue(g, codes, ring, bars, lane, nwarps);
+    prod.issue(g, codes, ring, nwarps, lane);
     cons.advance();
   }
-  wide |= emag >= (1u << 29);
+  wide |= dmag >= (1u << 28);
   if (__any_sync(FULL, wide)) {
     if (lane == 0) fa.redo_list[atomicAdd(fa.redo_count, 1u)] = tile;
     return;
@@ -298,20 +313,14 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, 4) dq_decompress_fast_kernel(
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   unsigned char* ring = smem_dfast + (size_t)wib * F::WARP_SMEM;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + FAST_STAGES * F::STAGE_BYTES + F::PREV_BYTES);
   const Geo& g = fa.d.g;
   const uint16_t* codes = reinterpret_cast<const uint16_t*>(fa.d.codes);
 
-  if (lane == 0) {
-    for (int s = 0; s < FAST_STAGES; ++s) mbar_init(&bars[s], 1);
-    fence_mbar_init();
-  }
-  __syncwarp();
   const uint32_t nwarps = gridDim.x * FAST_WARPS;
   const uint32_t first = blockIdx.x * FAST_WARPS + wib;
   DProducer<ND, B, VPL> prod;
-  prod.start(g, codes, first, nwarps);
-  for (int s = 0; s < FAST_STAGES; ++s) prod.issue(g, codes, ring, bars, lane, nwarps);
+  prod.start(g, codes, first, nwarps, lane);
+  for (int s = 0; s < FAST_STAGES; ++s) prod.issue(g, codes, ring, nwarps, lane);
   Consumer<ND, B, VPL> cons{0, 0u};
   long long sent = 0;
   for (uint32_t tile = first; tile < (uint32_t)g.ntiles; tile += nwarps) {
@@ -320,7 +329,7 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, 4) dq_decompress_fast_kernel(
       if (lane == 0) fa.redo_list[atomicAdd(fa.redo_count, 1u)] = tile;
       continue;
     }
-    dfast_tile<ND, B, VPL>(fa, tile, tc, lane, ring, bars, prod, cons, nwarps, sent);
+    dfast_tile<ND, B, VPL>(fa, tile, tc, lane, ring, prod, cons, nwarps, sent);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) sent += __shfl_xor_sync(FULL, sent, o);

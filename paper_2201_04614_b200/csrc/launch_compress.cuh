@@ -11,6 +11,40 @@
 
 namespace vlz {
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+inline EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// input float32 array as a (D2, D1, D0) uint32 tensor (bit-exact copies), box
+// (W, BY, 1): one plane of one tile; out-of-bounds elements read as zero
+inline bool make_plane_map(CUtensorMap* m, const float* in, const Geo& g, int W, int BY) {
+  EncodeTiledFn fn = encode_tiled();
+  if (!fn) return false;
+  if (g.D0 > 0xffffffffll || g.D1 > 0xffffffffll || g.D2 > 0xffffffffll) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)g.D2, (cuuint64_t)g.D1, (cuuint64_t)g.D0};
+  const cuuint64_t strides[2] = {(cuuint64_t)g.D2 * 4, (cuuint64_t)(g.D1 * g.D2) * 4};
+  const cuuint32_t box[3] = {(cuuint32_t)W, (cuuint32_t)BY, 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<float*>(in), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int ND, int B>
 constexpr bool has_fast() {
   return (ND == 3 || ND == 2) && (B == 8 || B == 16);
@@ -21,7 +55,9 @@ cudaError_t run_compress_shape(const CompressArgs& a, cudaStream_t st) {
   constexpr int smem = 4 * plane_smem_bytes<ND, B, VPL>();
   if constexpr (has_fast<ND, B>()) {
     const bool aligned = (a.g.D2 % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.in) & 15) == 0);
-    if (aligned && a.redo_list != nullptr && a.g.ntiles < (1ll << 30)) {
+    FastArgs fa{};
+    if (aligned && a.redo_list != nullptr && a.g.ntiles < (1ll << 30) &&
+        make_plane_map(&fa.tmap, a.in, a.g, Shape<ND, B, VPL>::W, Shape<ND, B, VPL>::BY)) {
       auto kern = dq_compress_fast_kernel<ND, B, VPL, MODE, K>;
       constexpr int fsmem = fast_smem_bytes<ND, B, VPL>();
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem);
@@ -34,7 +70,9 @@ cudaError_t run_compress_shape(const CompressArgs& a, cudaStream_t st) {
       const int64_t need = (a.g.ntiles + FAST_WARPS - 1) / FAST_WARPS;
       if (grid > need) grid = need;
       if (grid < 1) grid = 1;
-      FastArgs fa{a, const_cast<unsigned int*>(a.redo_count), const_cast<long long*>(a.redo_list)};
+      fa.c = a;
+      fa.redo_count = const_cast<unsigned int*>(a.redo_count);
+      fa.redo_list = const_cast<long long*>(a.redo_list);
       const bool t = g_timing.load(std::memory_order_relaxed);
       if (t) timing_mark(TK_COMPRESS, true, st);
       kern<<<(unsigned)grid, FAST_WARPS * 32, fsmem, st>>>(fa);
