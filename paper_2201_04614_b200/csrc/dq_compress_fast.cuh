@@ -39,6 +39,7 @@ struct FastShape {
   // ring of input planes + the previous plane's Dy Dx d (int32, 3-D only)
   static constexpr int PREV_BYTES = (ND == 3) ? PLANE_BYTES : 0;
   static constexpr int WARP_SMEM = (FAST_STAGES * PLANE_BYTES + PREV_BYTES + 64 + 127) / 128 * 128;
+  static constexpr int MINB = (VPL == 2) ? 6 : 4;  // CTAs per SM the register budget targets
 };
 
 template <int ND, int B, int VPL>
@@ -197,8 +198,8 @@ __device__ __forceinline__ void fast_tile(const FastArgs& fa, uint32_t tile, con
     int prow[VPL];
 #pragma unroll
     for (int j = 0; j < VPL; ++j) prow[j] = 0;  // Dy zero fill at the block's first row
-    long long psum = 0;
-#pragma unroll 1
+    int psum = 0;  // |sum of a plane| < BY * W / 32 * VPL * 2^24 < 2^31
+#pragma unroll 2
     for (int yl = 0; yl < BY; ++yl) {
       if (!INTERIOR && yl >= ey) break;
       float v[VPL];
@@ -225,9 +226,7 @@ __device__ __forceinline__ void fast_tile(const FastArgs& fa, uint32_t tile, con
         for (int j = 0; j < VPL; ++j)
           if (j >= nvalid) nb[j] = MAGIC_BITS;  // out-of-bounds columns act as d = 0
       }
-      bool bad[VPL];
-#pragma unroll
-      for (int j = 0; j < VPL; ++j) bad[j] = false;
+      unsigned badm = 0;  // narrowing-check failures (exact path only)
       if (!__all_sync(FULL, allok)) {
         // rare: exact float64 re-evaluation of the flagged elements, one at a
         // time (one inlined copy of quant_exact; operands picked by select)
@@ -247,10 +246,8 @@ __device__ __forceinline__ void fast_tile(const FastArgs& fa, uint32_t tile, con
           bool bj, ovf;
           const int nj = quant_exact(vj, q, bj, ovf);
 #pragma unroll
-          for (int k = 0; k < VPL; ++k) {
-            nb[k] = (j == k) ? (unsigned)nj + MAGIC_BITS : nb[k];
-            bad[k] = (j == k) ? bj : bad[k];
-          }
+          for (int k = 0; k < VPL; ++k) nb[k] = (j == k) ? (unsigned)nj + MAGIC_BITS : nb[k];
+          if (bj) badm |= 1u << j;
           if (ovf) {
             const unsigned long long fi =
                 (unsigned long long)(((z0 + zl) * g.D1 + (y0 + yl)) * g.D2 + xl0 + j);
@@ -298,14 +295,23 @@ __device__ __forceinline__ void fast_tile(const FastArgs& fa, uint32_t tile, con
 #pragma unroll
       for (int j = 0; j < VPL; ++j) {
         const int u = dl[j] + (R - 1);
-        out[j] = ((unsigned)u > span) || bad[j];
+        out[j] = (unsigned)u > span;
         c[j] = out[j] ? 0u : (uint32_t)(u + 1);
         anyout = anyout || out[j];
+      }
+      if (badm) {  // rare, lane-local: narrowed reconstruction misses the bound
+#pragma unroll
+        for (int j = 0; j < VPL; ++j)
+          if ((badm >> j) & 1u) {
+            out[j] = true;
+            c[j] = 0u;
+          }
+        anyout = true;
       }
       const bool origin_row = (zl == 0) && (yl == 0) && xhead;
       if (origin_row) {
         d_origin = (int)(nb[0] - MAGIC_BITS);
-        bad_origin = bad[0];
+        bad_origin = badm & 1u;
         v_origin = v[0];
       }
       if (vec_store) {
@@ -433,7 +439,7 @@ __device__ __forceinline__ void fast_tile(const FastArgs& fa, uint32_t tile, con
 }
 
 template <int ND, int B, int VPL, int MODE, int K>
-__global__ void __launch_bounds__(FAST_WARPS * 32, 4)
+__global__ void __launch_bounds__(FAST_WARPS * 32, (FastShape<ND, B, VPL>::MINB))
     dq_compress_fast_kernel(const __grid_constant__ FastArgs fa) {
   using S = Shape<ND, B, VPL>;
   using F = FastShape<ND, B, VPL>;

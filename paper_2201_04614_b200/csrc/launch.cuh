@@ -8,6 +8,10 @@
 
 #include "dq_decompress.cuh"
 
+#ifndef VLZ_VPL_3D8
+#define VLZ_VPL_3D8 4  // columns per lane for 3-D b=8 tiles (window 32*VPL)
+#endif
+
 namespace vlz {
 
 // total kernel launches issued by the library (evidence for bench.py)
@@ -56,6 +60,7 @@ inline int vpl_for(int nd, int B) {
   if (nd == 1 && B == 256) return 8;
   if (nd == 3 && B == 64) return 2;
   if (nd >= 2 && B == 16) return 2;
+  if (nd == 3 && B == 8) return VLZ_VPL_3D8;
   return 4;
 }
 
