@@ -335,6 +335,50 @@ int64_t vlzo_block_count(int nd, const int64_t* dims, int b) {
   return g.nblocks;
 }
 
+/* Slab-sharded runs (SURVEY 8c "full-size parity strategy"): a shard of a
+ * block-aligned slab must use the scalar of the WHOLE array for *:global
+ * policies, as if compute_padding had been handed the full field.  The test
+ * harness computes per-shard partial statistics with vlzo_global_stats,
+ * all-reduces them and injects the result here. */
+static int g_override_on = 0;
+static int64_t g_override_value = 0;
+
+void vlzo_set_global_scalar_override(int enable, int64_t value) {
+  g_override_on = enable;
+  g_override_value = value;
+}
+
+/* partial statistics of a slab's prequantized field: out = {wrapping sum,
+ * count, min, max}; returns a VLZO_* status (prequantize errors) */
+int vlzo_global_stats(const float* data, int64_t n, double eb, int64_t* out,
+                      int64_t* err_index) {
+  const size_t nn = (size_t)(n > 0 ? n : 1);
+  int64_t* dq = (int64_t*)malloc(nn * sizeof(int64_t));
+  if (!dq) return VLZO_NOMEM;
+  int rc = vlzo_prequantize(data, n, eb, dq, err_index);
+  if (rc == VLZO_OK) {
+    uint64_t sum = 0;
+    int64_t mn = INT64_MAX, mx = INT64_MIN;
+    for (int64_t i = 0; i < n; ++i) {
+      sum += (uint64_t)dq[i];
+      if (dq[i] < mn) mn = dq[i];
+      if (dq[i] > mx) mx = dq[i];
+    }
+    out[0] = (int64_t)sum;
+    out[1] = n;
+    out[2] = mn;
+    out[3] = mx;
+  }
+  free(dq);
+  return rc;
+}
+
+/* exact rounding of the global mean from reduced statistics (padding.py:53-69) */
+int64_t vlzo_stat_value(int kind, int64_t sum, int64_t count, int64_t mn, int64_t mx) {
+  stat_t s = {mn, mx, (uint64_t)sum, count};
+  return stat_value(&s, kind);
+}
+
 /*
  * Full dual-quant compress (vector.py:205-260 semantics, scalar evaluation).
  * codes: N uint32 (canonical order); outlier_vals: capacity N; counts: nblocks;
@@ -365,6 +409,7 @@ int vlzo_dualquant(const float* data, int nd, const int64_t* dims, int b, double
   int rc = vlzo_prequantize(data, n, eb, dq, err_index);
   if (rc != VLZO_OK) return rc;
   compute_padding(&g, dq, pad_kind, pad_gran, scalars);
+  if (g_override_on && pad_kind != PAD_ZERO && pad_gran == GRAN_GLOBAL) scalars[0] = g_override_value;
   const int64_t keep_max = radius - 1;
   const int64_t bmax = (int64_t)b * (nd > 1 ? b : 1) * (nd > 2 ? b : 1);
 
