@@ -275,6 +275,12 @@ def run_ours(args):
             t_d[0] += ev[1].elapsed_time(ev[2])
         return n_out
 
+    # clocks are sampled from the start of the warm-up through the end of the
+    # timed region (nvidia-smi needs ~0.5 s to start; both phases run the
+    # same kernels back to back)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.5)
     for _ in range(args.warmup):
         n_out = step(False)
     torch.cuda.synchronize()
@@ -290,13 +296,11 @@ def run_ours(args):
     err = (y.double() - x.double()).abs().max().item()
     assert err <= eb, f"bound violated {err} > {eb}"
 
-    clocks = ClockSampler(local)
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
     l0 = lib.vlz_launch_count()
     lib.vlz_timing(1)
-    clocks.start()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
