@@ -336,7 +336,9 @@ __device__ __forceinline__ bool compress_tile(const CompressArgs& a, int64_t til
         total += 1;
       }
     }
-    a.counts[bi] = total;  // *:global adds the origin in the finish kernel
+    // *:global: the origin is still pending -- hand the scan kernel its
+    // prequantized value and narrowing verdict packed beside the count
+    a.counts[bi] = (MODE == MODE_GLOBAL) ? pack_origin(total, d_origin, bad_origin) : total;
   }
   return false;
 }

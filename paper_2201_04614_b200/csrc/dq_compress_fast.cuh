@@ -36,10 +36,15 @@ struct FastShape {
   using S = Shape<ND, B, VPL>;
   static constexpr int PLANE_FLOATS = S::BY * S::W;
   static constexpr int PLANE_BYTES = PLANE_FLOATS * 4;
+  // a plane streams in SPLIT ring stages of STAGE_ROWS rows each
+  static constexpr int SPLIT = 1;
+  static constexpr int STAGE_ROWS = S::BY / SPLIT;
+  static constexpr int STAGE_FLOATS = STAGE_ROWS * S::W;
+  static constexpr int STAGE_BYTES = STAGE_FLOATS * 4;
   // ring of input planes + the previous plane's Dy Dx d (int32, 3-D only)
   static constexpr int PREV_BYTES = (ND == 3) ? PLANE_BYTES : 0;
-  static constexpr int WARP_SMEM = (FAST_STAGES * PLANE_BYTES + PREV_BYTES + 64 + 127) / 128 * 128;
-  static constexpr int MINB = (VPL == 2) ? 6 : 4;  // CTAs per SM the register budget targets
+  static constexpr int WARP_SMEM = (FAST_STAGES * STAGE_BYTES + PREV_BYTES + 64 + 127) / 128 * 128;
+  static constexpr int MINB = 4;  // CTAs per SM the register budget targets
 };
 
 template <int ND, int B, int VPL>
@@ -67,18 +72,19 @@ __device__ __forceinline__ TileXY decode_tile(const Geo& g, uint32_t tile) {
   return t;
 }
 
-// producer side of the per-warp plane ring: one TMA tensor load per plane
+// producer side of the per-warp ring: one TMA tensor load per half plane
 template <int ND, int B, int VPL>
 struct Producer {
   using S = Shape<ND, B, VPL>;
   uint32_t tile;  // current tile (>= ntiles: done)
-  int zl, ez;
+  int zl, ez, part;
   int x0, y0, z0;
   int stage;
 
   __device__ __forceinline__ void start(const Geo& g, uint32_t t) {
     tile = t;
     zl = 0;
+    part = 0;
     stage = 0;
     setup(g);
   }
@@ -97,10 +103,13 @@ struct Producer {
     if (tile >= (uint32_t)g.ntiles) return;
     if (lane == 0) {
       uint64_t* bar = &bars[stage];
-      mbar_arrive_expect_tx(bar, (uint32_t)F::PLANE_BYTES);
-      tma_load_3d(ring + stage * F::PLANE_FLOATS, tmap, x0, y0, z0 + zl, bar);
+      mbar_arrive_expect_tx(bar, (uint32_t)F::STAGE_BYTES);
+      tma_load_3d(ring + stage * F::STAGE_FLOATS, tmap, x0, y0 + part * F::STAGE_ROWS, z0 + zl,
+                  bar);
     }
     if (++stage == FAST_STAGES) stage = 0;
+    if (++part < F::SPLIT) return;
+    part = 0;
     if (++zl >= ez) {
       zl = 0;
       tile += nwarps;
@@ -174,7 +183,7 @@ __device__ __forceinline__ void fast_tile(const FastArgs& fa, uint32_t tile, con
   // magic-number bias there so that the biased bit patterns cancel exactly
   const bool xhead = (xin == 0);
 
-  int* const pplane = reinterpret_cast<int*>(ring + FAST_STAGES * F::PLANE_FLOATS) + lane * VPL;
+  int* const pplane = reinterpret_cast<int*>(ring + FAST_STAGES * F::STAGE_FLOATS) + lane * VPL;
   if (ND == 3) {  // previous-plane state starts at zero (Dz zero fill)
 #pragma unroll 1
     for (int yl = 0; yl < BY; ++yl) {
@@ -193,21 +202,23 @@ __device__ __forceinline__ void fast_tile(const FastArgs& fa, uint32_t tile, con
   uint16_t* cptr = a.codes + bstart + xin;  // advances by ex per row
 
   for (int zl = 0; zl < ez; ++zl) {
-    const float* plane = ring + cons.stage * F::PLANE_FLOATS + lane * VPL;
-    mbar_wait(&bars[cons.stage], cons.parity);
     int prow[VPL];
 #pragma unroll
     for (int j = 0; j < VPL; ++j) prow[j] = 0;  // Dy zero fill at the block's first row
     int psum = 0;  // |sum of a plane| < BY * W / 32 * VPL * 2^24 < 2^31
+    for (int part = 0; part < F::SPLIT; ++part) {
+    const float* plane = ring + cons.stage * F::STAGE_FLOATS + lane * VPL;
+    mbar_wait(&bars[cons.stage], cons.parity);
 #pragma unroll 2
-    for (int yl = 0; yl < BY; ++yl) {
+    for (int r = 0; r < F::STAGE_ROWS; ++r) {
+      const int yl = part * F::STAGE_ROWS + r;
       if (!INTERIOR && yl >= ey) break;
       float v[VPL];
       if (VPL == 4) {
-        const float4 f = *reinterpret_cast<const float4*>(plane + yl * W);
+        const float4 f = *reinterpret_cast<const float4*>(plane + r * W);
         v[0] = f.x; v[1 % VPL] = f.y; v[2 % VPL] = f.z; v[3 % VPL] = f.w;
       } else {
-        const float2 f = *reinterpret_cast<const float2*>(plane + yl * W);
+        const float2 f = *reinterpret_cast<const float2*>(plane + r * W);
         v[0] = f.x; v[1 % VPL] = f.y;
       }
       // ---- float32 fast prequantization; nb = biased bit pattern of n
@@ -376,15 +387,16 @@ __device__ __forceinline__ void fast_tile(const FastArgs& fa, uint32_t tile, con
         }
       }
     }
-    if (MODE == MODE_GLOBAL) {
-      tacc.sum += psum;
-      tcnt += (long long)nvalid * ey;
-    }
-    // release the slot and refill it FAST_STAGES planes ahead
+    // release the stage and refill it FAST_STAGES half planes ahead
     __syncwarp();
     fence_proxy_async_smem();
     prod.issue(g, &fa.tmap, ring, bars, lane, nwarps);
     cons.advance();
+    }
+    if (MODE == MODE_GLOBAL) {
+      tacc.sum += psum;
+      tcnt += (long long)nvalid * ey;
+    }
   }
 
   // int32 stencil may have wrapped: hand the whole tile to the int64 redo
@@ -434,7 +446,9 @@ __device__ __forceinline__ void fast_tile(const FastArgs& fa, uint32_t tile, con
         total += 1;
       }
     }
-    a.counts[bi] = total;
+    // *:global: the origin is still pending -- hand the scan kernel its
+    // prequantized value and narrowing verdict packed beside the count
+    a.counts[bi] = (MODE == MODE_GLOBAL) ? pack_origin(total, d_origin, bad_origin) : total;
   }
 }
 
@@ -448,7 +462,7 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, (FastShape<ND, B, VPL>::MINB)
   const int wib = threadIdx.x >> 5;
   float* ring = reinterpret_cast<float*>(smem_fast + (size_t)wib * F::WARP_SMEM);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_fast + (size_t)wib * F::WARP_SMEM +
-                                               FAST_STAGES * F::PLANE_BYTES + F::PREV_BYTES);
+                                               FAST_STAGES * F::STAGE_BYTES + F::PREV_BYTES);
   const Geo& g = fa.c.g;
 
   if (lane == 0) {

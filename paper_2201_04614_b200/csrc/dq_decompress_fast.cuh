@@ -307,8 +307,7 @@ __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, c
 }
 
 template <int ND, int B, int VPL>
-__global__ void __launch_bounds__(FAST_WARPS * 32, (FastShape<ND, B, VPL>::MINB))
-    dq_decompress_fast_kernel(DFastArgs fa) {
+__global__ void __launch_bounds__(FAST_WARPS * 32, 4) dq_decompress_fast_kernel(DFastArgs fa) {
   using F = DFastShape<ND, B, VPL>;
   extern __shared__ __align__(128) unsigned char smem_dfast[];
   const int lane = threadIdx.x & 31;

@@ -49,14 +49,26 @@ struct ScanArgs {
   long long* index;
   const unsigned long long* first_nonfinite;
   const unsigned long long* first_overflow;
+  // optional list of rewritten origin codes, (position << 16) | code, for
+  // callers that copied the provisional codes out early (host pipeline)
+  unsigned long long* patch_list;
+  unsigned int* patch_count;
 };
 
 __device__ __forceinline__ void block_of(const Geo& g, int64_t bi, int BZ, int BY, int BX,
                                          int64_t& bstart, int64_t& origin) {
-  const int64_t bx = bi % g.P2;
-  const int64_t t = bi / g.P2;
-  const int64_t by = t % g.P1;
-  const int64_t bz = t / g.P1;
+  int64_t bx, by, bz;
+  if (g.nblocks < 0xffffffffll) {  // 32-bit magic division (the common case)
+    const uint32_t t = g.divP2.div((uint32_t)bi);
+    bx = (uint32_t)bi - t * (uint32_t)g.P2;
+    bz = g.divP1.div(t);
+    by = t - (uint32_t)bz * (uint32_t)g.P1;
+  } else {
+    bx = bi % g.P2;
+    const int64_t t = bi / g.P2;
+    by = t % g.P1;
+    bz = t / g.P1;
+  }
   const int64_t ez = imin64(BZ, g.D0 - bz * BZ);
   const int64_t ey = imin64(BY, g.D1 - by * BY);
   bstart = block_start(g, bz, by, bx, BZ, BY, BX, ez, ey);
@@ -99,15 +111,28 @@ __global__ void __launch_bounds__(SCAN_THREADS) dq_scan_kernel(ScanArgs a) {
         int64_t bstart, origin;
         block_of(a.g, bi, a.BZ, a.BY, a.BX, bstart, origin);
         if (a.fix_origin) {
-          bool bad, ovf;
-          const float v = a.in[origin];
-          const int d = quant_exact(v, a.q, bad, ovf);
+          // pending-origin record written by the fused kernel (pack_origin)
+          const int64_t rec = c[k];
+          const int d = (int)(rec >> 32);
+          const bool bad = (rec >> 24) & 1;
+          c[k] = rec & 0xffffff;
           const int64_t delta = (int64_t)d - s0;
           const int R = a.q.radius;
           const bool out = bad || delta > (int64_t)(R - 1) || delta < -(int64_t)(R - 1);
-          a.codes[bstart] = out ? (uint16_t)0 : (uint16_t)(delta + R);
+          const uint16_t code = out ? (uint16_t)0 : (uint16_t)(delta + R);
+          // the fused kernel already stored the s0 = 0 code of the origin;
+          // rewrite only when s0 changes it (saves a sector read-modify-write
+          // per block when the global scalar is 0)
+          const bool out0 = bad || d > R - 1 || d < -(R - 1);
+          const uint16_t code0 = out0 ? (uint16_t)0 : (uint16_t)(d + R);
+          if (code != code0) {
+            a.codes[bstart] = code;
+            if (a.patch_list)
+              a.patch_list[atomicAdd(a.patch_count, 1u)] =
+                  ((unsigned long long)bstart << 16) | (unsigned long long)code;
+          }
           if (out) {
-            a.scratch[bstart] = v;
+            a.scratch[bstart] = a.in[origin];  // verbatim value, read only for outliers
             c[k] += 1;
           }
           a.counts[bi] = c[k];

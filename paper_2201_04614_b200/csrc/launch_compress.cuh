@@ -31,7 +31,7 @@ inline EncodeTiledFn encode_tiled() {
 }
 
 // input float32 array as a (D2, D1, D0) uint32 tensor (bit-exact copies), box
-// (W, BY, 1): one plane of one tile; out-of-bounds elements read as zero
+// (W, rows, 1): part of one plane of one tile; out-of-bounds elements read as zero
 inline bool make_plane_map(CUtensorMap* m, const float* in, const Geo& g, int W, int BY) {
   EncodeTiledFn fn = encode_tiled();
   if (!fn) return false;
@@ -57,7 +57,8 @@ cudaError_t run_compress_shape(const CompressArgs& a, cudaStream_t st) {
     const bool aligned = (a.g.D2 % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.in) & 15) == 0);
     FastArgs fa{};
     if (aligned && a.redo_list != nullptr && a.g.ntiles < (1ll << 30) &&
-        make_plane_map(&fa.tmap, a.in, a.g, Shape<ND, B, VPL>::W, Shape<ND, B, VPL>::BY)) {
+        make_plane_map(&fa.tmap, a.in, a.g, Shape<ND, B, VPL>::W,
+                       FastShape<ND, B, VPL>::STAGE_ROWS)) {
       auto kern = dq_compress_fast_kernel<ND, B, VPL, MODE, K>;
       constexpr int fsmem = fast_smem_bytes<ND, B, VPL>();
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem);

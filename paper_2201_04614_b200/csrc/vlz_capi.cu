@@ -102,6 +102,7 @@ bool make_geo(const vlz_geom* gg, Geo& g) {
   g.N = D[0] * D[1] * D[2];
   g.divNW.init((uint32_t)(g.NW < 0xffffffffll ? g.NW : 1));
   g.divP1.init((uint32_t)(g.P1 < 0xffffffffll ? g.P1 : 1));
+  g.divP2.init((uint32_t)(g.P2 < 0xffffffffll ? g.P2 : 1));
   return true;
 }
 
@@ -319,7 +320,7 @@ size_t vlz_workspace_size(const vlz_geom* gg) {
   return carve(g, null_base).bytes;
 }
 
-static int compress_begin_impl(const float* d_in, const vlz_geom* gg, const vlz_params* p,
+__attribute__((visibility("hidden"))) int vlz_internal_compress_begin(const float* d_in, const vlz_geom* gg, const vlz_params* p,
                                uint16_t* d_codes, int64_t* d_counts, int64_t* d_scalars,
                                vlz_result* d_result, long long* stats, void* d_ws,
                                size_t ws_bytes, cudaStream_t st) {
@@ -358,10 +359,11 @@ static int compress_begin_impl(const float* d_in, const vlz_geom* gg, const vlz_
   return to_rc(e);
 }
 
-static int compress_finish_impl(const float* d_in, const vlz_geom* gg, const vlz_params* p,
+__attribute__((visibility("hidden"))) int vlz_internal_compress_finish(const float* d_in, const vlz_geom* gg, const vlz_params* p,
                                 const long long* gstats, uint16_t* d_codes, float* d_outliers,
                                 int64_t* d_counts, int64_t* d_scalars, vlz_result* d_result,
-                                void* d_ws, size_t ws_bytes, cudaStream_t st) {
+                                void* d_ws, size_t ws_bytes, cudaStream_t st,
+                                unsigned long long* patch_list, unsigned int* patch_count) {
   Geo g;
   if (!make_geo(gg, g) || !valid_params(p) || !d_outliers || !d_result || !d_ws)
     return VLZ_E_ARG;
@@ -391,6 +393,8 @@ static int compress_finish_impl(const float* d_in, const vlz_geom* gg, const vlz
   s.index = reinterpret_cast<long long*>(&d_result->index);
   s.first_nonfinite = reinterpret_cast<const unsigned long long*>(&d_result->first_nonfinite);
   s.first_overflow = reinterpret_cast<const unsigned long long*>(&d_result->first_overflow);
+  s.patch_list = patch_list;
+  s.patch_count = patch_count;
   if (mode == MODE_GLOBAL && !gstats) return VLZ_E_ARG;
   return to_rc(launch_scan(s, st));
 }
@@ -402,18 +406,18 @@ int vlz_dq_compress(const float* d_in, const vlz_geom* g, const vlz_params* p, u
   Geo gg;
   if (!make_geo(g, gg)) return VLZ_E_ARG;
   WS w = carve(gg, d_ws);
-  int rc = compress_begin_impl(d_in, g, p, d_codes, d_counts, d_scalars, d_result, w.stats,
+  int rc = vlz_internal_compress_begin(d_in, g, p, d_codes, d_counts, d_scalars, d_result, w.stats,
                                d_ws, ws_bytes, st);
   if (rc != VLZ_OK) return rc;
-  return compress_finish_impl(d_in, g, p, w.stats, d_codes, d_outliers, d_counts, d_scalars,
-                              d_result, d_ws, ws_bytes, st);
+  return vlz_internal_compress_finish(d_in, g, p, w.stats, d_codes, d_outliers, d_counts, d_scalars,
+                              d_result, d_ws, ws_bytes, st, nullptr, nullptr);
 }
 
 int vlz_dq_compress_begin(const float* d_in, const vlz_geom* g, const vlz_params* p,
                           uint16_t* d_codes, int64_t* d_counts, int64_t* d_scalars,
                           vlz_result* d_result, vlz_stats* d_stats, void* d_ws, size_t ws_bytes,
                           void* stream) {
-  return compress_begin_impl(d_in, g, p, d_codes, d_counts, d_scalars, d_result,
+  return vlz_internal_compress_begin(d_in, g, p, d_codes, d_counts, d_scalars, d_result,
                              reinterpret_cast<long long*>(d_stats), d_ws, ws_bytes,
                              static_cast<cudaStream_t>(stream));
 }
@@ -422,12 +426,12 @@ int vlz_dq_compress_finish(const float* d_in, const vlz_geom* g, const vlz_param
                            const vlz_stats* d_global_stats, uint16_t* d_codes, float* d_outliers,
                            int64_t* d_counts, int64_t* d_scalars, vlz_result* d_result,
                            void* d_ws, size_t ws_bytes, void* stream) {
-  return compress_finish_impl(d_in, g, p, reinterpret_cast<const long long*>(d_global_stats),
+  return vlz_internal_compress_finish(d_in, g, p, reinterpret_cast<const long long*>(d_global_stats),
                               d_codes, d_outliers, d_counts, d_scalars, d_result, d_ws,
-                              ws_bytes, static_cast<cudaStream_t>(stream));
+                              ws_bytes, static_cast<cudaStream_t>(stream), nullptr, nullptr);
 }
 
-static int decompress_impl(const void* d_codes, bool u32, const float* d_outliers,
+__attribute__((visibility("hidden"))) int vlz_internal_decompress(const void* d_codes, bool u32, const float* d_outliers,
                            int64_t n_outliers, const int64_t* d_counts, const int64_t* d_scalars,
                            const vlz_geom* gg, const vlz_params* p, float* d_out,
                            vlz_result* d_result, void* d_ws, size_t ws_bytes, cudaStream_t st) {
@@ -485,7 +489,7 @@ int vlz_dq_decompress(const uint16_t* d_codes, const float* d_outliers, int64_t 
                       const int64_t* d_counts, const int64_t* d_scalars, const vlz_geom* g,
                       const vlz_params* p, float* d_out, vlz_result* d_result, void* d_ws,
                       size_t ws_bytes, void* stream) {
-  return decompress_impl(d_codes, false, d_outliers, n_outliers, d_counts, d_scalars, g, p, d_out,
+  return vlz_internal_decompress(d_codes, false, d_outliers, n_outliers, d_counts, d_scalars, g, p, d_out,
                          d_result, d_ws, ws_bytes, static_cast<cudaStream_t>(stream));
 }
 
@@ -493,7 +497,7 @@ int vlz_dq_decompress_u32(const uint32_t* d_codes, const float* d_outliers, int6
                           const int64_t* d_counts, const int64_t* d_scalars, const vlz_geom* g,
                           const vlz_params* p, float* d_out, vlz_result* d_result, void* d_ws,
                           size_t ws_bytes, void* stream) {
-  return decompress_impl(d_codes, true, d_outliers, n_outliers, d_counts, d_scalars, g, p, d_out,
+  return vlz_internal_decompress(d_codes, true, d_outliers, n_outliers, d_counts, d_scalars, g, p, d_out,
                          d_result, d_ws, ws_bytes, static_cast<cudaStream_t>(stream));
 }
 
@@ -520,129 +524,6 @@ int vlz_minmax(const float* d_in, int64_t n, double* d_minmax, void* stream) {
   minmax_kernel<<<(unsigned)blocks, 256, 0, st>>>(d_in, n, w, w + 1, w + 2, w + 3, d_minmax);
   g_launches.fetch_add(2, std::memory_order_relaxed);
   return to_rc(cudaGetLastError());
-}
-
-// ---- host-buffer entry points ------------------------------------------
-namespace {
-struct HostCache {
-  int dev = -1;
-  cudaStream_t st = nullptr;
-  void* buf = nullptr;
-  size_t cap = 0;
-};
-HostCache g_host[64];
-std::mutex g_host_mu;
-
-void* host_buffer(int dev, size_t need, cudaStream_t& st) {
-  HostCache& c = g_host[dev];
-  if (!c.st) cudaStreamCreateWithFlags(&c.st, cudaStreamNonBlocking);
-  if (c.cap < need) {
-    if (c.buf) cudaFree(c.buf);
-    c.buf = nullptr;
-    c.cap = 0;
-    if (cudaMalloc(&c.buf, need) != cudaSuccess) return nullptr;
-    c.cap = need;
-  }
-  st = c.st;
-  return c.buf;
-}
-}  // namespace
-
-int vlz_dq_compress_host(const float* h_in, const vlz_geom* gg, const vlz_params* p,
-                         uint16_t* h_codes, float* h_outliers, int64_t* h_counts,
-                         int64_t* h_scalars, vlz_result* h_result, int device) {
-  Geo g;
-  if (!make_geo(gg, g) || !valid_params(p) || device < 0 || device >= 64) return VLZ_E_ARG;
-  std::lock_guard<std::mutex> lk(g_host_mu);
-  int prev = 0;
-  cudaGetDevice(&prev);
-  cudaSetDevice(device);
-  const int64_t ns = vlz_scalar_count(gg, p->pad_kind, p->pad_gran);
-  const size_t ws = vlz_workspace_size(gg);
-  const size_t o_in = 0, o_codes = align256(g.N * 4), o_out = o_codes + align256(g.N * 2),
-               o_cnt = o_out + align256(g.N * 4), o_sc = o_cnt + align256(g.nblocks * 8),
-               o_res = o_sc + align256((ns > 0 ? ns : 1) * 8), o_ws = o_res + 256,
-               total = o_ws + ws;
-  cudaStream_t st;
-  char* base = static_cast<char*>(host_buffer(device, total, st));
-  if (!base) {
-    cudaSetDevice(prev);
-    return VLZ_E_CUDA;
-  }
-  float* d_in = reinterpret_cast<float*>(base + o_in);
-  uint16_t* d_codes = reinterpret_cast<uint16_t*>(base + o_codes);
-  float* d_out = reinterpret_cast<float*>(base + o_out);
-  int64_t* d_cnt = reinterpret_cast<int64_t*>(base + o_cnt);
-  int64_t* d_sc = reinterpret_cast<int64_t*>(base + o_sc);
-  vlz_result* d_res = reinterpret_cast<vlz_result*>(base + o_res);
-  cudaMemcpyAsync(d_in, h_in, g.N * 4, cudaMemcpyHostToDevice, st);
-  int rc = vlz_dq_compress(d_in, gg, p, d_codes, d_out, d_cnt, d_sc, d_res, base + o_ws, ws, st);
-  if (rc == VLZ_OK) {
-    cudaMemcpyAsync(h_result, d_res, sizeof(vlz_result), cudaMemcpyDeviceToHost, st);
-    cudaMemcpyAsync(h_codes, d_codes, g.N * 2, cudaMemcpyDeviceToHost, st);
-    cudaMemcpyAsync(h_counts, d_cnt, g.nblocks * 8, cudaMemcpyDeviceToHost, st);
-    if (ns > 0) cudaMemcpyAsync(h_scalars, d_sc, ns * 8, cudaMemcpyDeviceToHost, st);
-    cudaError_t e = cudaStreamSynchronize(st);
-    if (e == cudaSuccess && h_result->status == VLZ_ST_OK && h_result->n_outliers > 0) {
-      cudaMemcpyAsync(h_outliers, d_out, h_result->n_outliers * 4, cudaMemcpyDeviceToHost, st);
-      e = cudaStreamSynchronize(st);
-    }
-    rc = to_rc(e);
-  }
-  cudaSetDevice(prev);
-  return rc;
-}
-
-int vlz_dq_decompress_host(const uint16_t* h_codes, const float* h_outliers, int64_t n_outliers,
-                           const int64_t* h_counts, const int64_t* h_scalars, const vlz_geom* gg,
-                           const vlz_params* p, float* h_out, vlz_result* h_result, int device) {
-  Geo g;
-  if (!make_geo(gg, g) || !valid_params(p) || device < 0 || device >= 64 || n_outliers < 0)
-    return VLZ_E_ARG;
-  std::lock_guard<std::mutex> lk(g_host_mu);
-  int prev = 0;
-  cudaGetDevice(&prev);
-  cudaSetDevice(device);
-  const int64_t ns = vlz_scalar_count(gg, p->pad_kind, p->pad_gran);
-  const size_t ws = vlz_workspace_size(gg);
-  const size_t o_codes = 0, o_ol = align256(g.N * 2), o_cnt = o_ol + align256(n_outliers * 4 + 4),
-               o_sc = o_cnt + align256(g.nblocks * 8),
-               o_out = o_sc + align256((ns > 0 ? ns : 1) * 8), o_res = o_out + align256(g.N * 4),
-               o_ws = o_res + 256, total = o_ws + ws;
-  cudaStream_t st;
-  char* base = static_cast<char*>(host_buffer(device, total, st));
-  if (!base) {
-    cudaSetDevice(prev);
-    return VLZ_E_CUDA;
-  }
-  uint16_t* d_codes = reinterpret_cast<uint16_t*>(base + o_codes);
-  float* d_ol = reinterpret_cast<float*>(base + o_ol);
-  int64_t* d_cnt = reinterpret_cast<int64_t*>(base + o_cnt);
-  int64_t* d_sc = reinterpret_cast<int64_t*>(base + o_sc);
-  float* d_out = reinterpret_cast<float*>(base + o_out);
-  vlz_result* d_res = reinterpret_cast<vlz_result*>(base + o_res);
-  cudaMemcpyAsync(d_codes, h_codes, g.N * 2, cudaMemcpyHostToDevice, st);
-  if (n_outliers > 0) cudaMemcpyAsync(d_ol, h_outliers, n_outliers * 4, cudaMemcpyHostToDevice, st);
-  cudaMemcpyAsync(d_cnt, h_counts, g.nblocks * 8, cudaMemcpyHostToDevice, st);
-  if (ns > 0) cudaMemcpyAsync(d_sc, h_scalars, ns * 8, cudaMemcpyHostToDevice, st);
-  int rc = vlz_dq_decompress(d_codes, d_ol, n_outliers, d_cnt, d_sc, gg, p, d_out, d_res,
-                             base + o_ws, ws, st);
-  if (rc == VLZ_OK) {
-    cudaMemcpyAsync(h_result, d_res, sizeof(vlz_result), cudaMemcpyDeviceToHost, st);
-    cudaMemcpyAsync(h_out, d_out, g.N * 4, cudaMemcpyDeviceToHost, st);
-    rc = to_rc(cudaStreamSynchronize(st));
-  }
-  cudaSetDevice(prev);
-  return rc;
-}
-
-void vlz_host_release(void) {
-  std::lock_guard<std::mutex> lk(g_host_mu);
-  for (auto& c : g_host) {
-    if (c.buf) cudaFree(c.buf);
-    c.buf = nullptr;
-    c.cap = 0;
-  }
 }
 
 int64_t vlz_launch_count(void) { return g_launches.load(); }

@@ -53,7 +53,7 @@ struct Geo {
   int64_t ntiles;      // P0 * P1 * NW
   int64_t nblocks;
   int64_t N;
-  FastDiv divNW, divP1;  // 32-bit tile decode (valid when ntiles < 2^31)
+  FastDiv divNW, divP1, divP2;  // 32-bit tile / block decode (when counts < 2^32)
 };
 
 struct QP {
@@ -130,6 +130,13 @@ __device__ __forceinline__ int64_t quant_value(float v, double twoeb) {
 // quantize.py:45-47: float32((2.0 * d) * eb)
 __device__ __forceinline__ float dequant(int64_t d, double eb) {
   return __double2float_rn(__dmul_rn(2.0 * (double)d, eb));
+}
+
+// Pending-origin record of a block (fused compress -> scan, *:global only):
+// bits 0-23 outliers of the block's other elements, bit 24 the origin's
+// narrowing-check failure, bits 32-63 the origin's prequantized value.
+__host__ __device__ __forceinline__ int64_t pack_origin(int64_t count, int d, bool bad) {
+  return (int64_t)(((uint64_t)(uint32_t)d << 32) | ((uint64_t)bad << 24) | (uint64_t)count);
 }
 
 // padding.py:53-59 (total is the int64 wrapping sum)
