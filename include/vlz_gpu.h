@@ -161,6 +161,28 @@ int vlz_dq_decompress_host(const uint16_t* h_codes, const float* h_outliers,
 /* release the cached staging buffers of the host entry points */
 void vlz_host_release(void);
 
+/* ---- entropy stage after the path (huffman.py, container.py) ------------ *
+ * canonical Huffman coding of the uint16 code stream with the reference's
+ * codebook, bit order and error verdicts (see csrc/huffman.cpp). */
+/* symbol frequencies (np.bincount, huffman.py:62) on the device; d_freqs is
+ * uint64[65536]; radius centres the shared-memory window */
+int vlz_histogram(const uint16_t* d_codes, int64_t n, int32_t radius, uint64_t* d_freqs,
+                  void* stream);
+void vlz_histogram_host(const uint16_t* h_codes, int64_t n, uint64_t* h_freqs);
+/* build_codebook (huffman.py:56-88): canonical (length, symbol) order; returns
+ * 0, -1 for an empty stream, -2 if a code length exceeds 64 bits */
+int vlz_huff_build(const uint64_t* h_freqs, uint16_t* h_syms, uint8_t* h_lens, int32_t* h_nsym);
+/* encode (huffman.py:91-122): MSB-first; returns 0 or -1 (*bad_symbol set) */
+int vlz_huff_encode(const uint16_t* h_codes, int64_t n, const uint16_t* h_syms,
+                    const uint8_t* h_lens, int32_t nsym, uint8_t* h_out, int64_t out_cap,
+                    int64_t* h_nbits, int64_t* h_bad_symbol);
+/* decode (huffman.py:125-207): exactly `count` symbols; returns 0 or the
+ * reference's verdict 1..5 (empty/short payload/underrun/invalid prefix/
+ * consumed != declared bits) */
+int vlz_huff_decode(const uint8_t* h_payload, int64_t nbytes, int64_t bit_length,
+                    const uint16_t* h_syms, const uint8_t* h_lens, int32_t nsym, int64_t count,
+                    uint16_t* h_out, int64_t* h_consumed);
+
 /* number of kernel launches the library issued since load (bench evidence) */
 int64_t vlz_launch_count(void);
 /* per-kernel CUDA-event timing: when enabled every launch is bracketed by

@@ -63,6 +63,13 @@ PROTOTYPES = {
     "vlz_dq_decompress_host": (ctypes.c_int, [_vp, _vp, _i64, _vp, _vp, _P(Geom), _P(Params), _vp,
                                               _P(Result), ctypes.c_int]),
     "vlz_host_release": (None, []),
+    "vlz_histogram": (ctypes.c_int, [_vp, _i64, ctypes.c_int32, _vp, _vp]),
+    "vlz_histogram_host": (None, [_vp, _i64, _vp]),
+    "vlz_huff_build": (ctypes.c_int, [_vp, _vp, _vp, _P(ctypes.c_int32)]),
+    "vlz_huff_encode": (ctypes.c_int, [_vp, _i64, _vp, _vp, ctypes.c_int32, _vp, _i64, _P(_i64),
+                                       _P(_i64)]),
+    "vlz_huff_decode": (ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, ctypes.c_int32, _i64, _vp,
+                                       _P(_i64)]),
     "vlz_launch_count": (_i64, []),
     "vlz_timing": (None, [ctypes.c_int]),
     "vlz_timing_collect": (ctypes.c_int, [_P(ctypes.c_double), _P(_i64), ctypes.c_int]),

@@ -247,5 +247,16 @@ def check_decompress(result: torch.Tensor, codes, counts, n_outliers, grid, radi
     raise RuntimeError(f"unexpected decompress status {r.status}")
 
 
+def histogram_device(codes: torch.Tensor, radius: int = 512, stream=None) -> np.ndarray:
+    """uint64[65536] frequencies of a uint16 (int16 storage) CUDA code tensor."""
+    lib = _lib.load()
+    freqs = torch.empty(65536, dtype=torch.int64, device=codes.device)
+    c = codes.contiguous()
+    rc = lib.vlz_histogram(_ptr(c), c.numel(), int(radius), _ptr(freqs), _stream(stream))
+    if rc != 0:
+        raise RuntimeError(f"vlz_histogram failed ({rc})")
+    return freqs.cpu().numpy().view(np.uint64)
+
+
 def launch_count() -> int:
     return int(_lib.load().vlz_launch_count())

@@ -1,0 +1,98 @@
+"""End-to-end entry points of the drop-in (reference pipeline.py:16-32,
+reconstruct.py:74-129).
+
+    blob = compress(data, config)          # float32 ndarray -> VLZ1 bytes
+    arr, desc = decompress(blob)           # VLZ1 bytes -> float32 ndarray
+
+Both run the dual-quant path on the GPU (libvlzgpu.so); the entropy stage
+(histogram on the GPU, canonical Huffman codebook + MSB-first coding natively
+on the host) and the container framing produce the reference's exact bytes.
+`lane_width` 1 and the vector lane widths give the same bytes, as in the
+reference (its scalar and vector kernels are byte-identical).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import gpu
+from .container import ParsedContainer, deserialize, serialize_parts
+from .errors import BoundTooSmallError, ConfigError
+from .huffman import build_codebook_from_freqs, decode, encode
+from .model import (
+    ArrayDescriptor,
+    CodeStream,
+    CompressionConfig,
+    PaddingScalars,
+    build_block_grid,
+    resolve_error_bound,
+)
+from .reconstruct import reconstruct_arrays
+
+__all__ = ["compress", "compress_detailed", "decompress", "decompress_parsed"]
+
+
+def _device():
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2201_04614_b200 needs a CUDA device (B200); no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _compress(data: np.ndarray, config: CompressionConfig, want_stream: bool):
+    desc = ArrayDescriptor.from_array(data)
+    eb = resolve_error_bound(config.error_bound, data)
+    grid = build_block_grid(desc, config.block_edge)
+    if eb <= 0.0:
+        raise ConfigError(f"resolved error bound must be > 0, got {eb}")
+    x = torch.from_numpy(np.ascontiguousarray(data)).to(_device())
+    dev = gpu.compress_device(x, config, eb=eb)
+    try:
+        dev.check()
+    except BoundTooSmallError as exc:
+        raise BoundTooSmallError(exc.index, float(data.ravel()[exc.index]), eb) from None
+    n_out = dev.n_outliers
+    freqs = gpu.histogram_device(dev.codes[: desc.element_count], config.radius)
+    codebook = build_codebook_from_freqs(freqs)
+    codes16 = dev.codes[: desc.element_count].cpu().numpy().view(np.uint16)
+    bits, nbits = encode(codes16, codebook)
+    outliers = dev.outliers[:n_out].cpu().numpy()
+    counts = dev.counts[: grid.block_count].cpu().numpy()
+    scalars = dev.scalars.cpu().numpy().astype(np.int64)
+    blob = serialize_parts(desc, config, eb, config.radius, codebook, bits, nbits, scalars,
+                           counts, outliers, grid.block_count)
+    stream = None
+    if want_stream:
+        stream = CodeStream(codes=codes16.astype(np.uint32), outlier_values=outliers,
+                            outlier_counts=counts, grid=grid, resolved_abs=eb,
+                            radius=config.radius,
+                            scalars=PaddingScalars(config.padding, scalars))
+    return blob, stream
+
+
+def compress(data: np.ndarray, config: CompressionConfig) -> bytes:
+    """pipeline.py:16-23: float32 array -> container bytes."""
+    return _compress(data, config, want_stream=False)[0]
+
+
+def compress_detailed(data: np.ndarray, config: CompressionConfig):
+    """pipeline.py:26-32: (container bytes, CodeStream)."""
+    return _compress(data, config, want_stream=True)
+
+
+def decompress_parsed(parsed: ParsedContainer, thread_count: int = 1):
+    """reconstruct.py:74-124: Huffman decode, then the GPU block reconstruction
+    (thread_count is accepted for compatibility and ignored)."""
+    desc = parsed.descriptor
+    grid = build_block_grid(desc, parsed.block_edge)
+    codes = decode(parsed.code_bits, parsed.code_bit_length, parsed.codebook,
+                   desc.element_count)
+    out = reconstruct_arrays(codes, parsed.outlier_values, parsed.outlier_counts,
+                             parsed.padding_values, grid, parsed.resolved_abs, parsed.radius,
+                             parsed.padding_policy)
+    return out, desc
+
+
+def decompress(blob: bytes, thread_count: int = 1):
+    """reconstruct.py:127-129: container bytes -> (float32 array, descriptor)."""
+    return decompress_parsed(deserialize(blob), thread_count=thread_count)

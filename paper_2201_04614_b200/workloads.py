@@ -101,7 +101,7 @@ def gen_c4(n: int = 512, seed: int = 4) -> np.ndarray:
     kk[0, 0, 0] = 1.0
     f *= kk ** (-1.5)
     f[0, 0, 0] = 0.0
-    g = np.fft.irfftn(f, s=(n, n, n))
+    g = np.fft.irfftn(f, s=(n, n, n), axes=(0, 1, 2))
     g /= g.std()
     return np.exp(g).astype(np.float32)
 

@@ -322,6 +322,100 @@ def make_known():
     print(f"wrote known.json: {len(cases)} cases")
 
 
+def make_container():
+    """Reference deserialize/decode verdicts on mutated containers
+    (container.py:166-298, huffman.py:125-207; test_container.py:118-131)."""
+    from vlz.huffman import decode as hdecode
+
+    rng = np.random.default_rng(77)
+    blobs = []
+    d = _smooth(rng, (13, 11))
+    blobs.append(compress(d, _cfg(1e-4, 8, "mean:block", 32768)))
+    d2 = _noise(rng, (9, 10, 7))
+    blobs.append(compress(d2, _cfg(1e-3, 8, "zero", 512)))
+    cases = []
+
+    def verdict(blob):
+        try:
+            parsed = deserialize(blob)
+            hdecode(parsed.code_bits, parsed.code_bit_length, parsed.codebook,
+                    parsed.descriptor.element_count)
+        except verr.VlzError as exc:
+            return {"type": type(exc).__name__, "message": str(exc)}
+        return None
+
+    import struct
+    import zlib
+
+    H = struct.Struct("<4sHHBBBB3QddHHIQ5QI")
+
+    def fix_crc(b: bytes) -> bytes:
+        f = list(H.unpack_from(b, 0))
+        total = f[20]
+        body = b[H.size: len(b) - 4]
+        hdr = H.pack(*f[:-1], 0)
+        hdr = H.pack(*f[:-1], zlib.crc32(hdr))
+        return hdr + body + struct.pack("<I", zlib.crc32(body)) if total == len(b) else \
+            hdr + b[H.size:]
+
+    def set_field(b: bytes, idx: int, val) -> bytes:
+        f = list(H.unpack_from(b, 0))
+        f[idx] = val
+        return fix_crc(H.pack(*f) + b[H.size:])
+
+    def patch(b: bytes, off: int, new: bytes) -> bytes:
+        return fix_crc(b[:off] + new + b[off + len(new):])
+
+    for bi, blob in enumerate(blobs):
+        f = H.unpack_from(blob, 0)
+        off_pad, off_cb, off_codes, off_out = f[16:20]
+        muts = [("truncate_half", blob[: len(blob) // 2]), ("truncate_small", blob[:50]),
+                ("bad_magic", b"XLZ1" + blob[4:]),
+                ("version", blob[:4] + (2).to_bytes(2, "little") + blob[6:]),
+                ("header_flip", blob[:40] + bytes([blob[40] ^ 1]) + blob[41:]),
+                ("payload_flip", blob[:-10] + bytes([blob[-10] ^ 0x10]) + blob[-9:]),
+                ("extra_byte", blob + b"\x00"),
+                # structured edits with both CRCs recomputed: deeper validation
+                ("ndims4", set_field(blob, 3, 4)),
+                ("eb_mode", set_field(blob, 4, 7)),
+                ("pad_kind", set_field(blob, 5, 9)),
+                ("block12", set_field(blob, 12, 12)),
+                ("elemcount", set_field(blob, 15, f[15] + 1)),
+                ("dim0", set_field(blob, 7, f[7] + 1)),
+                ("offsets_swap", set_field(set_field(blob, 17, f[18]), 18, f[17])),
+                ("off_pad", set_field(blob, 16, f[16] + 8)),
+                ("radius_small", set_field(blob, 14, 2)),
+                ("sym_big", patch(blob, off_cb + 4, struct.pack("<H", 65535))),
+                ("len_zero", patch(blob, off_cb + 6, b"\x00")),
+                ("nbits_plus", patch(blob, off_codes, struct.pack("<Q",
+                                   struct.unpack_from("<Q", blob, off_codes)[0] + 1))),
+                ("nbits_minus", patch(blob, off_codes, struct.pack("<Q",
+                                    struct.unpack_from("<Q", blob, off_codes)[0] - 3))),
+                ("nbits_huge", patch(blob, off_codes, struct.pack("<Q", 1 << 40))),
+                ("nout_plus", patch(blob, off_out, struct.pack("<Q",
+                                  struct.unpack_from("<Q", blob, off_out)[0] + 1))),
+                ("nz_huge", patch(blob, off_out + 8, struct.pack("<Q", 1 << 30))),
+                ("padcount_huge", patch(blob, off_pad, struct.pack("<Q", 1 << 30)))]
+        nz = struct.unpack_from("<Q", blob, off_out + 8)[0]
+        if nz:
+            muts.append(("pair_block_oob", patch(blob, off_out + 16, struct.pack("<I", 1 << 20))))
+            muts.append(("pair_count", patch(blob, off_out + 20, struct.pack("<I", 999))))
+        nbytes = (struct.unpack_from("<Q", blob, off_codes)[0] + 7) // 8
+        for k in range(12):  # flips inside the Huffman payload, CRCs fixed
+            pos = off_codes + 8 + int(rng.integers(0, nbytes))
+            muts.append((f"bits{k}", patch(blob, pos, bytes([blob[pos] ^ int(rng.integers(1, 256))]))))
+        for k in range(25):
+            b = bytearray(blob)
+            pos = int(rng.integers(0, len(b)))
+            b[pos] ^= int(rng.integers(1, 256))
+            muts.append((f"fuzz{k}", bytes(b)))
+        for tag, m in muts:
+            cases.append(dict(tag=f"b{bi}_{tag}", blob=m.hex(), expect=verdict(m)))
+    with open(os.path.join(HERE, "container.json"), "w") as fh:
+        json.dump(cases, fh)
+    print(f"wrote container.json: {len(cases)} cases")
+
+
 def _sha(a):
     return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
 
@@ -348,6 +442,6 @@ def make_fullsize():
 
 
 if __name__ == "__main__":
-    what = sys.argv[1:] or ["corpus", "errors", "corrupt", "known", "fullsize"]
+    what = sys.argv[1:] or ["corpus", "errors", "corrupt", "known", "fullsize", "container"]
     for w in what:
         globals()[f"make_{w}"]()
