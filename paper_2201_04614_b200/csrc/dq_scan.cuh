@@ -24,8 +24,20 @@
 namespace vlz {
 
 constexpr int SCAN_THREADS = 256;
-constexpr int SCAN_IPT = 8;
-constexpr int SCAN_CH = SCAN_THREADS * SCAN_IPT;
+constexpr int SCAN_MIN_CH = SCAN_THREADS;  // smallest chunk (blocks per CTA)
+
+// blocks per thread: 8 for large grids (few look-back steps), fewer when the
+// grid is small so that the outlier gather still spreads over >= ~4 CTAs/SM
+inline int scan_ipt(int64_t nblocks) {
+  int ipt = 1;
+  while (ipt < 8 && nblocks > (int64_t)SCAN_THREADS * ipt * 148 * 4) ipt *= 2;
+  return ipt;
+}
+inline int64_t scan_chunks(int64_t nblocks) {
+  const int64_t ch = (int64_t)SCAN_THREADS * scan_ipt(nblocks);
+  const int64_t n = (nblocks + ch - 1) / ch;
+  return n < 1 ? 1 : n;
+}
 
 struct ScanArgs {
   Geo g;
@@ -79,8 +91,9 @@ constexpr unsigned long long FLAG_A = 1ull << 62;
 constexpr unsigned long long FLAG_P = 2ull << 62;
 constexpr unsigned long long VAL_MASK = (1ull << 62) - 1;
 
+template <int SCAN_IPT>
 __global__ void __launch_bounds__(SCAN_THREADS) dq_scan_kernel(ScanArgs a) {
-  __shared__ long long s_inc[SCAN_CH];   // chunk-local inclusive prefix per block
+  constexpr int SCAN_CH = SCAN_THREADS * SCAN_IPT;
   __shared__ long long s_src[SCAN_CH];   // scratch source of each block's outliers
   __shared__ long long s_warp[SCAN_THREADS / 32];
   __shared__ long long s_excl;
@@ -208,32 +221,54 @@ __global__ void __launch_bounds__(SCAN_THREADS) dq_scan_kernel(ScanArgs a) {
   __syncthreads();
   const long long cexcl = s_excl;
 
-  // per-block offsets
+  // per-block offsets (decompress) or outlier gather (compress): each thread
+  // copies the outliers of its own blocks -- all copies of the chunk are in
+  // flight at once -- and blocks with >= 32 outliers are copied by the whole
+  // warp, coalesced
   long long run = texcl;
+  unsigned heavy = 0;
+  long long hdst[SCAN_IPT];
 #pragma unroll
   for (int k = 0; k < SCAN_IPT; ++k) {
     const int64_t bi = base + (int64_t)tid * SCAN_IPT + k;
+    const long long dst = cexcl + run;
+    hdst[k] = dst;
     if (!a.gather) {
-      if (bi < nb) a.offsets[bi] = cexcl + run;
+      if (bi < nb) a.offsets[bi] = dst;
+    } else if (c[k] > 0 && c[k] < 32) {
+      const float* src = a.scratch + s_src[tid * SCAN_IPT + k];
+      for (long long t = 0; t < c[k]; ++t) a.out[dst + t] = src[t];
+    } else if (c[k] >= 32) {
+      heavy |= 1u << k;
     }
     run += c[k];
-    s_inc[tid * SCAN_IPT + k] = run;
   }
   if (!a.gather) return;
-  __syncthreads();
-
-  // cooperative gather of this chunk's outliers
-  const long long T = agg;
-  for (long long t = tid; t < T; t += SCAN_THREADS) {
-    // first k with s_inc[k] > t
-    int lo = 0, hi = SCAN_CH - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (s_inc[mid] > t) hi = mid;
-      else lo = mid + 1;
+  unsigned hm = __ballot_sync(FULL, heavy != 0);
+  while (hm) {
+    const int src_lane = __ffs(hm) - 1;
+    hm &= hm - 1;
+    const unsigned mk = __shfl_sync(FULL, heavy, src_lane);
+#pragma unroll
+    for (int k = 0; k < SCAN_IPT; ++k) {
+      if (!((mk >> k) & 1u)) continue;  // warp-uniform
+      const long long n = __shfl_sync(FULL, c[k], src_lane);
+      const long long dst = __shfl_sync(FULL, hdst[k], src_lane);
+      const float* src = a.scratch + s_src[(tid - lane + src_lane) * SCAN_IPT + k];
+      for (long long t0 = 0; t0 < n; t0 += 128) {
+        float v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const long long t = t0 + lane + 32 * j;
+          if (t < n) v[j] = __ldg(src + t);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const long long t = t0 + lane + 32 * j;
+          if (t < n) a.out[dst + t] = v[j];
+        }
+      }
     }
-    const long long kexcl = lo ? s_inc[lo - 1] : 0;
-    a.out[cexcl + t] = a.scratch[s_src[lo] + (t - kexcl)];
   }
 }
 

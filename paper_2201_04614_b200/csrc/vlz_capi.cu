@@ -144,7 +144,7 @@ WS carve(const Geo& g, void* base) {
   w.stats = reinterpret_cast<long long*>(p + off + 64);
   w.aux = reinterpret_cast<long long*>(p + off + 128);
   off += 256;
-  const int64_t nchunks = (g.nblocks + SCAN_CH - 1) / SCAN_CH;
+  const int64_t nchunks = (g.nblocks + SCAN_MIN_CH - 1) / SCAN_MIN_CH;
   w.lb = reinterpret_cast<unsigned long long*>(p + off);
   off += align256((size_t)nchunks * 8);
   w.redo_list = reinterpret_cast<long long*>(p + off);
@@ -200,12 +200,17 @@ cudaError_t launch_init(vlz_result* res, const WS& w, long long* stats, int64_t 
 }
 
 cudaError_t launch_scan(const ScanArgs& a, cudaStream_t st) {
-  int64_t nchunks = (a.g.nblocks + SCAN_CH - 1) / SCAN_CH;
-  if (nchunks < 1) nchunks = 1;
+  const int64_t nchunks = scan_chunks(a.g.nblocks);
+  const int ipt = scan_ipt(a.g.nblocks);
   const bool t = g_timing.load(std::memory_order_relaxed);
   const int kind = a.gather ? TK_SCAN_C : TK_SCAN_D;
   if (t) timing_mark(kind, true, st);
-  dq_scan_kernel<<<(unsigned)nchunks, SCAN_THREADS, 0, st>>>(a);
+  switch (ipt) {
+    case 1: dq_scan_kernel<1><<<(unsigned)nchunks, SCAN_THREADS, 0, st>>>(a); break;
+    case 2: dq_scan_kernel<2><<<(unsigned)nchunks, SCAN_THREADS, 0, st>>>(a); break;
+    case 4: dq_scan_kernel<4><<<(unsigned)nchunks, SCAN_THREADS, 0, st>>>(a); break;
+    default: dq_scan_kernel<8><<<(unsigned)nchunks, SCAN_THREADS, 0, st>>>(a); break;
+  }
   if (t) timing_mark(kind, false, st);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
@@ -333,7 +338,7 @@ __attribute__((visibility("hidden"))) int vlz_internal_compress_begin(const floa
   const int mode = mode_of(p->pad_kind, p->pad_gran);
   if (mode != MODE_ZERO && !d_scalars) return VLZ_E_ARG;
   if (mode == MODE_GLOBAL && !stats) return VLZ_E_ARG;
-  const int64_t nchunks = (g.nblocks + SCAN_CH - 1) / SCAN_CH;
+  const int64_t nchunks = scan_chunks(g.nblocks);
   cudaError_t e = launch_init(d_result, w, stats, nchunks, st);
   if (e != cudaSuccess) return to_rc(e);
   CompressArgs a{};
@@ -443,7 +448,7 @@ __attribute__((visibility("hidden"))) int vlz_internal_decompress(const void* d_
   if (ws_bytes < w.bytes) return VLZ_E_ARG;
   const int mode = mode_of(p->pad_kind, p->pad_gran);
   if (mode != MODE_ZERO && !d_scalars) return VLZ_E_ARG;
-  const int64_t nchunks = (g.nblocks + SCAN_CH - 1) / SCAN_CH;
+  const int64_t nchunks = scan_chunks(g.nblocks);
   cudaError_t e = launch_init(d_result, w, nullptr, nchunks, st);
   if (e != cudaSuccess) return to_rc(e);
   const int b = gg->block_edge;
