@@ -14,8 +14,13 @@
 //    E = d - s0 of each element is a signed sum of 7 earlier exact values
 //    (each < 2^28) plus a code (< 2^15), so it lies in (-2^31, 2^31) where
 //    congruence mod 2^32 is equality.  The kernel checks exactly that and
-//    hands any tile that fails it -- and every edge tile -- to the int64
-//    kernel (dq_decompress_kernel<..., LIST=true>);
+//    hands any tile that fails it to the int64 kernel
+//    (dq_decompress_kernel<..., LIST=true>);
+//  * edge tiles (partial last block row / window) run afterwards in
+//    dq_decompress_edge_kernel, the same recurrence instantiated with EDGE:
+//    codes are fetched synchronously (partial blocks are not 4-byte aligned)
+//    and positions beyond the array read as "delta 0" -- they trail every
+//    valid position of their block in x and y, so they never feed one;
 //  * output rows leave with 16-byte stores straight from registers.
 #pragma once
 
@@ -108,7 +113,7 @@ struct DProducer {
   }
 };
 
-template <int ND, int B, int VPL>
+template <int ND, int B, int VPL, bool EDGE>
 __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, const TileXY& tc,
                                            int lane, unsigned char* ring,
                                            DProducer<ND, B, VPL>& prod,
@@ -130,17 +135,25 @@ __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, c
   const int64_t bxg = (int64_t)tc.wx * F::NBLK + blk;
   const int64_t bi = ((int64_t)tc.bz * g.P1 + tc.by) * g.P2 + bxg;
   const int gl = lane & (LPB - 1);
+  // edge tiles: valid rows, valid columns of this lane's block (<= 0: the
+  // block lies beyond the array and the lane only carries zeros)
+  const int ey = EDGE ? (int)imin64(BY, g.D1 - y0) : BY;
+  const int ex = EDGE ? (int)imax64(0, imin64(BX, g.D2 - bxg * BX)) : BX;
+  const bool bvalid = !EDGE || ex > 0;
 
   int s0 = 0;
   bool wide = false;
   long long s064 = 0;
-  if (a.mode == MODE_GLOBAL) s064 = a.scalars[0];
-  else if (a.mode == MODE_BLOCK) s064 = a.scalars[bi];
-  else if (a.mode == MODE_EDGE) s064 = a.scalars[bi * a.nd];
+  long long off = 0, avail = 0;
+  if (bvalid) {
+    if (a.mode == MODE_GLOBAL) s064 = a.scalars[0];
+    else if (a.mode == MODE_BLOCK) s064 = a.scalars[bi];
+    else if (a.mode == MODE_EDGE) s064 = a.scalars[bi * a.nd];
+    off = a.offsets[bi];
+    avail = imax64(0, imin64(a.counts[bi], a.n_outliers - off));
+  }
   wide |= (s064 >= (1ll << 27)) || (s064 <= -(1ll << 27));
   s0 = (int)s064;
-  const long long off = a.offsets[bi];
-  const long long avail = imax64(0, imin64(a.counts[bi], a.n_outliers - off));
 
   // The outermost prefix state is primed with s0 (3-D: the previous-plane
   // state starts at s0; 1-D/2-D: the previous-row state does), so d = E + s0
@@ -160,16 +173,38 @@ __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, c
   float* orow = a.out + (z0 * g.D1 + y0) * g.D2 + xl0;
   const unsigned char* const slot0 = ring + lane * F::LANE_BYTES;
 
+  const uint16_t* esrc = nullptr;
+  if (EDGE) esrc = codes + block_start(g, tc.bz, tc.by, bxg, BZ, BY, BX, ez, ey) + xin;
   for (int zl = 0; zl < ez; ++zl) {
-    const unsigned char* slot = slot0 + cons.stage * F::STAGE_BYTES;
-    cp_async_wait<FAST_STAGES - 1>();
+    const unsigned char* slot;
+    if (EDGE) {
+      // synchronous fill of stage 0: invalid positions read as code R
+      unsigned char* fill = ring + lane * F::LANE_BYTES;
+      const uint16_t* zs = esrc + (int64_t)zl * ey * ex;
+#pragma unroll
+      for (int yl = 0; yl < BY; ++yl) {
+        unsigned v[VPL];
+#pragma unroll
+        for (int j = 0; j < VPL; ++j)
+          v[j] = (yl < ey && xin + j < ex) ? (unsigned)zs[yl * ex + j] : (unsigned)R;
+        if (VPL == 4)
+          *reinterpret_cast<uint2*>(fill + yl * 32 * F::LANE_BYTES) =
+              make_uint2(v[0] | (v[1 % VPL] << 16), v[2 % VPL] | (v[3 % VPL] << 16));
+        else
+          *reinterpret_cast<unsigned*>(fill + yl * 32 * F::LANE_BYTES) = v[0] | (v[1 % VPL] << 16);
+      }
+      slot = slot0;
+    } else {
+      slot = slot0 + cons.stage * F::STAGE_BYTES;
+      cp_async_wait<FAST_STAGES - 1>();
+    }
     int grow[VPL];
 #pragma unroll
     for (int j = 0; j < VPL; ++j) grow[j] = (ND == 3) ? 0 : s0;
     int* pp = pplane;
     float* dst = orow;
 #pragma unroll 1
-    for (int yl = 0; yl < BY; ++yl) {
+    for (int yl = 0; yl < ey; ++yl) {
       unsigned c[VPL];
       if (VPL == 4) {
         const uint2 pk = *reinterpret_cast<const uint2*>(slot);
@@ -282,13 +317,18 @@ __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, c
         else *reinterpret_cast<int2*>(pp) = make_int2(dv[0], dv[1 % VPL]);
       }
       pp += W;
-      if (VPL == 4) *reinterpret_cast<float4*>(dst) = make_float4(o[0], o[1 % VPL], o[2 % VPL], o[3 % VPL]);
-      else *reinterpret_cast<float2*>(dst) = make_float2(o[0], o[1 % VPL]);
+      // (D2 % 4 == 0: a lane's VPL columns are all inside or all outside)
+      if (!EDGE || xl0 < g.D2) {
+        if (VPL == 4) *reinterpret_cast<float4*>(dst) = make_float4(o[0], o[1 % VPL], o[2 % VPL], o[3 % VPL]);
+        else *reinterpret_cast<float2*>(dst) = make_float2(o[0], o[1 % VPL]);
+      }
       dst += g.D2;
     }
     orow += g.D1 * g.D2;
-    prod.issue(g, codes, ring, nwarps, lane);
-    cons.advance();
+    if (!EDGE) {
+      prod.issue(g, codes, ring, nwarps, lane);
+      cons.advance();
+    }
   }
   wide |= dmag >= (1u << 28);
   if (__any_sync(FULL, wide)) {
@@ -296,7 +336,7 @@ __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, c
     return;
   }
   const bool bad_any = group_any<LPB>(badcode, lane);
-  if (xin == 0) {
+  if (xin == 0 && bvalid) {
     sent_acc += run;
     int st = 0;
     if (bad_any) st = 4;
@@ -325,11 +365,54 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, 4) dq_decompress_fast_kernel(
   long long sent = 0;
   for (uint32_t tile = first; tile < (uint32_t)g.ntiles; tile += nwarps) {
     const TileXY tc = decode_tile(g, tile);
-    if (!tile_interior<ND, B, VPL>(g, tc)) {
-      if (lane == 0) fa.redo_list[atomicAdd(fa.redo_count, 1u)] = tile;
-      continue;
+    if (!tile_interior<ND, B, VPL>(g, tc)) continue;  // dq_decompress_edge_kernel
+    dfast_tile<ND, B, VPL, false>(fa, tile, tc, lane, ring, prod, cons, nwarps, sent);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sent += __shfl_xor_sync(FULL, sent, o);
+  if (lane == 0 && sent) atomicAdd(fa.d.sentinels, (unsigned long long)sent);
+}
+
+// edge tiles: the last window of every block row when W does not divide D2,
+// and every window of the last block row when BY does not divide D1
+template <int ND, int B, int VPL>
+__host__ __device__ inline int64_t edge_tile_count(const Geo& g) {
+  using S = Shape<ND, B, VPL>;
+  const bool xp = (g.D2 % S::W) != 0, yp = (g.D1 % S::BY) != 0;
+  return (xp ? g.P0 * g.P1 : 0) + (yp ? g.P0 * (g.NW - (xp ? 1 : 0)) : 0);
+}
+
+template <int ND, int B, int VPL>
+__global__ void __launch_bounds__(FAST_WARPS * 32, 4) dq_decompress_edge_kernel(DFastArgs fa) {
+  using S = Shape<ND, B, VPL>;
+  using F = DFastShape<ND, B, VPL>;
+  extern __shared__ __align__(128) unsigned char smem_dfast[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  unsigned char* ring = smem_dfast + (size_t)wib * F::WARP_SMEM;
+  const Geo& g = fa.d.g;
+  const bool xp = (g.D2 % S::W) != 0;
+  const int64_t na = xp ? g.P0 * g.P1 : 0;
+  const int64_t nxb = g.NW - (xp ? 1 : 0);
+  const int64_t n = edge_tile_count<ND, B, VPL>(g);
+  const int64_t nwarps = (int64_t)gridDim.x * FAST_WARPS;
+  DProducer<ND, B, VPL> prod{};
+  Consumer<ND, B, VPL> cons{0, 0u};
+  long long sent = 0;
+  for (int64_t i = (int64_t)blockIdx.x * FAST_WARPS + wib; i < n; i += nwarps) {
+    TileXY tc;
+    if (i < na) {
+      tc.bz = (uint32_t)(i / g.P1);
+      tc.by = (uint32_t)(i % g.P1);
+      tc.wx = (uint32_t)(g.NW - 1);
+    } else {
+      const int64_t j = i - na;
+      tc.bz = (uint32_t)(j / nxb);
+      tc.by = (uint32_t)(g.P1 - 1);
+      tc.wx = (uint32_t)(j % nxb);
     }
-    dfast_tile<ND, B, VPL>(fa, tile, tc, lane, ring, prod, cons, nwarps, sent);
+    const uint32_t tile = (uint32_t)(((int64_t)tc.bz * g.P1 + tc.by) * g.NW + tc.wx);
+    dfast_tile<ND, B, VPL, true>(fa, tile, tc, lane, ring, prod, cons, (uint32_t)nwarps, sent);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) sent += __shfl_xor_sync(FULL, sent, o);

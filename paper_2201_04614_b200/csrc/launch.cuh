@@ -21,7 +21,7 @@ int num_sms();
 
 // optional per-kernel CUDA-event timing (vlz_timing / vlz_timing_collect)
 enum TimedKind { TK_INIT = 0, TK_COMPRESS = 1, TK_SCAN_C = 2, TK_SCAN_D = 3, TK_DECOMPRESS = 4,
-                 TK_MINMAX = 5, TK_REDO = 6, TK_COUNT = 8 };
+                 TK_MINMAX = 5, TK_REDO = 6, TK_EDGE = 7, TK_COUNT = 8 };
 extern std::atomic<int> g_timing;
 void timing_mark(int kind, bool start, cudaStream_t st);
 

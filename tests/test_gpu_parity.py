@@ -225,3 +225,19 @@ def test_int64_redo_path(oracle):
     d = (rng.uniform(-1, 1, (40, 33, 70)) * 1.0e9).astype(np.float32)
     for pol in ("mean:global", "zero", "max:block", "min:edge"):
         _check_full(oracle, d, 0.9, 8, pol, 32768)
+
+
+@pytest.mark.parametrize("shape,b", [((21, 44, 260), 8), ((19, 44, 196), 16),
+                                     ((45, 300), 8), ((37, 196), 16), ((9, 12, 132), 8)])
+def test_fast_kernel_edge_tiles(oracle, shape, b):
+    # D2 % 4 == 0 keeps the fast decompress kernel eligible; the last window
+    # of every block row (W = 128 or 64 columns) and the last block row are
+    # partial, so dq_decompress_edge_kernel runs, with outliers and sentinels
+    rng = np.random.default_rng(sum(shape) + b)
+    idx = np.indices(shape).astype(np.float64)
+    smooth = sum(np.sin(0.07 * (k + 1) * idx[k]) * 40.0 for k in range(len(shape)))
+    data = (smooth + rng.normal(0, 0.05, shape)).astype(np.float32)
+    data.ravel()[rng.integers(0, data.size, 50)] *= 7.0  # spikes -> outliers
+    for eb, pol in ((1e-3, "mean:global"), (1e-4, "zero"), (1e-3, "max:block")):
+        s = _check_full(oracle, data, eb, b, pol, 512)
+        assert s.outlier_values.size > 0

@@ -39,7 +39,7 @@ def timed(fn, flush, reps):
         lib.vlz_timing_collect(kms, kc, 8)
         ts.append(a.elapsed_time(b))
         kt.append(dict(init=kms[0], compress=kms[1], scan_c=kms[2], scan_d=kms[3],
-                       decompress=kms[4], redo=kms[6]))
+                       decompress=kms[4], redo=kms[6], edge=kms[7]))
     i = ts.index(statistics.median(ts))
     return ts[i], kt[i]
 
