@@ -176,6 +176,22 @@ int vlz_huff_build(const uint64_t* h_freqs, uint16_t* h_syms, uint8_t* h_lens, i
 int vlz_huff_encode(const uint16_t* h_codes, int64_t n, const uint16_t* h_syms,
                     const uint8_t* h_lens, int32_t nsym, uint8_t* h_out, int64_t out_cap,
                     int64_t* h_nbits, int64_t* h_bad_symbol);
+/* device encode (huffman.py:91-122 on the GPU, csrc/k_huffenc.cu).
+ * vlz_huff_table uploads a canonical book (symbols/lengths in (length,
+ * symbol) order, lengths <= 58) into d_table (vlz_huff_table_bytes()).
+ * vlz_huff_encode_device packs n uint16 codes (16-byte aligned) into d_out
+ * (4-byte aligned, out_cap bytes; whole 32-bit words are written, bits past
+ * the end are zero) and fills d_info (int64[4], device): [0] bit length,
+ * [1] (index << 16 | symbol) of the first symbol >= nsym_span (= largest book
+ * symbol + 1) or INT64_MAX, [2] 1 if out_cap was too small, [3] first symbol
+ * absent from the book or INT64_MAX.  Stream-ordered, no host sync. */
+size_t vlz_huff_table_bytes(void);
+int vlz_huff_table(const uint16_t* h_syms, const uint8_t* h_lens, int32_t nsym, void* d_table,
+                   void* stream);
+size_t vlz_huff_encode_ws_size(int64_t n);
+int vlz_huff_encode_device(const uint16_t* d_codes, int64_t n, const void* d_table,
+                           int32_t nsym_span, uint8_t* d_out, int64_t out_cap, int64_t* d_info,
+                           void* d_ws, size_t ws_bytes, void* stream);
 /* decode (huffman.py:125-207): exactly `count` symbols; returns 0 or the
  * reference's verdict 1..5 (empty/short payload/underrun/invalid prefix/
  * consumed != declared bits) */

@@ -123,7 +123,16 @@ int vlz_huff_encode(const uint16_t* codes, int64_t n, const uint16_t* syms, cons
     const uint16_t s = codes[i];
     const int L = len_of[s];
     if (L == 0) {
+      // huffman.py:102-104: a symbol beyond the largest codebook symbol is
+      // reported first (anywhere in the stream), else the first absent one
+      int span = 0;
+      for (int k = 0; k < nsym; ++k) span = syms[k] + 1 > span ? syms[k] + 1 : span;
       *bad_symbol = s;
+      for (int64_t j = 0; j < n; ++j)
+        if (codes[j] >= span) {
+          *bad_symbol = codes[j];
+          break;
+        }
       return -1;
     }
     uint64_t c = code_of[s];

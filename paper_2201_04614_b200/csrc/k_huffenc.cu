@@ -1,0 +1,276 @@
+// k_huffenc.cu -- canonical Huffman encoding of the code stream on the GPU
+// (the reference's encode, huffman.py:91-122: MSB-first codewords packed back
+// to back, np.packbits zero-pads the last byte).
+//
+// One pass, no memset of the output:
+//  * a chunk of HE_CH symbols per CTA (dynamic ticket order); every thread
+//    looks up the (codeword, length) of its 16 symbols in the device table;
+//  * block scan of the lengths + decoupled look-back (lookback.cuh) give the
+//    chunk's global bit offset;
+//  * the chunk assembles its bits in shared memory, aligned to the global
+//    32-bit word grid (shared atomicOr; each thread flushes a register word
+//    only when it moves to the next word);
+//  * a chunk OWNS the output words whose first bit lies inside its bit range;
+//    the one word it shares with the next chunk is completed by reading that
+//    chunk's leading symbols (<= 31 bits, every codeword has >= 1 bit), so
+//    each word is written exactly once, with a plain coalesced store
+//    (byte-swapped: bit 0 of the stream is the MSB of byte 0).
+// Codewords up to 58 bits are supported (table entry = codeword << 6 | len);
+// a stream needs > 10^12 symbols before a Huffman code can be that deep.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "../../include/vlz_gpu.h"
+#include "launch.cuh"
+#include "lookback.cuh"
+
+namespace vlz {
+namespace {
+
+constexpr int HE_THREADS = 256;
+constexpr int HE_SPT = 16;                  // symbols per thread
+constexpr int HE_CH = HE_THREADS * HE_SPT;  // symbols per chunk
+constexpr int HE_MAXLEN = 58;
+constexpr int HE_WORDS = (HE_CH * HE_MAXLEN + 31) / 32 + 2;
+constexpr long long HE_NONE = 0x7fffffffffffffffll;
+
+struct HEArgs {
+  const uint16_t* codes;
+  int64_t n;
+  const unsigned long long* tab;  // [65536] codeword << 6 | length, 0 = absent
+  int32_t nsym_span;              // max codebook symbol + 1 (huffman.py:96)
+  uint32_t* out;
+  int64_t out_words;
+  unsigned long long* lb;
+  unsigned int* ticket;
+  long long* info;  // [0] bits, [1] first symbol >= span, [2] overflow, [3] first absent symbol
+};
+
+__global__ void he_init_kernel(unsigned long long* lb, int64_t nchunks, unsigned int* ticket,
+                               long long* info) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0) {
+    *ticket = 0;
+    info[0] = 0;
+    info[1] = HE_NONE;
+    info[2] = 0;
+    info[3] = HE_NONE;
+  }
+  for (int64_t k = i; k < nchunks; k += (int64_t)gridDim.x * blockDim.x) lb[k] = 0;
+}
+
+__global__ void he_table_kernel(const unsigned long long* staged, int32_t nsym,
+                                unsigned long long* tab) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nsym) tab[staged[2 * i]] = staged[2 * i + 1];
+}
+
+__global__ void __launch_bounds__(HE_THREADS) huff_encode_kernel(HEArgs a) {
+  __shared__ uint32_t s_words[HE_WORDS];
+  __shared__ int s_warp[HE_THREADS / 32];
+  __shared__ long long s_start;
+  __shared__ unsigned int s_tile;
+
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) s_tile = atomicAdd(a.ticket, 1u);
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const int64_t base = tile * HE_CH;
+  const int64_t i0 = base + (int64_t)tid * HE_SPT;
+
+  // ---- symbols -> (codeword, length)
+  unsigned sym[HE_SPT];
+  if (i0 + HE_SPT <= a.n) {
+    const uint4* v = reinterpret_cast<const uint4*>(a.codes + i0);
+    const uint4 w0 = v[0], w1 = v[1];
+    const unsigned ws[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      sym[2 * k] = ws[k] & 0xffffu;
+      sym[2 * k + 1] = ws[k] >> 16;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < HE_SPT; ++k) sym[k] = (i0 + k < a.n) ? a.codes[i0 + k] : 0xffffffffu;
+  }
+  unsigned long long ent[HE_SPT];
+  int tbits = 0;
+#pragma unroll
+  for (int k = 0; k < HE_SPT; ++k) {
+    ent[k] = 0;
+    if (sym[k] != 0xffffffffu) {
+      ent[k] = __ldg(a.tab + sym[k]);
+      if ((ent[k] & 63) == 0) {  // not in the codebook (reported, contributes no bits)
+        const long long tag = ((i0 + k) << 16) | (long long)sym[k];
+        atomicMin(&a.info[(int)sym[k] >= a.nsym_span ? 1 : 3], tag);
+      }
+    }
+    tbits += (int)(ent[k] & 63);
+  }
+
+  // ---- chunk scan of bit lengths
+  int inc = tbits;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += u;
+  }
+  if (lane == 31) s_warp[wid] = inc;
+  __syncthreads();
+  int wbase = 0, agg = 0;
+#pragma unroll
+  for (int w = 0; w < HE_THREADS / 32; ++w) {
+    if (w < wid) wbase += s_warp[w];
+    agg += s_warp[w];
+  }
+  const int texcl = wbase + inc - tbits;
+  if (wid == 0) {
+    const long long excl = lookback_exclusive(a.lb, tile, agg, lane);
+    if (lane == 0) {
+      s_start = excl;
+      if (base + HE_CH >= a.n) a.info[0] = excl + agg;
+    }
+  }
+  __syncthreads();
+  const long long start = s_start;
+  const int sh = (int)(start & 31);
+  const int e_local = sh + agg;
+  const int nwords = (e_local + 31) / 32;
+  for (int w = tid; w < nwords; w += HE_THREADS) s_words[w] = 0;
+  __syncthreads();
+
+  // ---- assemble this chunk's bits (aligned to the global word grid)
+  {
+    int p = sh + texcl;
+    int cur = p >> 5;
+    uint32_t acc = 0;
+#pragma unroll
+    for (int k = 0; k < HE_SPT; ++k) {
+      int L = (int)(ent[k] & 63);
+      if (L == 0) continue;
+      unsigned long long X = (ent[k] >> 6) << (64 - L);  // left-aligned codeword
+      while (L > 0) {
+        const int o = p & 31, w = p >> 5;
+        const int take = L < 32 - o ? L : 32 - o;
+        const uint32_t bits = (uint32_t)(X >> (64 - take));
+        if (w != cur) {
+          if (acc) atomicOr(&s_words[cur], acc);
+          cur = w;
+          acc = 0;
+        }
+        acc |= bits << (32 - o - take);
+        X <<= take;
+        L -= take;
+        p += take;
+      }
+    }
+    if (acc) atomicOr(&s_words[cur], acc);
+  }
+  __syncthreads();
+
+  // ---- complete the last (shared) word from the next chunk's leading symbols
+  if (wid == 0 && (e_local & 31) && base + HE_CH < a.n) {
+    const int64_t i = base + HE_CH + lane;
+    unsigned long long e = 0;
+    if (i < a.n) e = __ldg(a.tab + a.codes[i]);
+    const int L = (int)(e & 63);
+    int x = L;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += u;
+    }
+    const int excl = x - L;
+    const int need = 32 - (e_local & 31);
+    if (L > 0 && excl < need) {
+      const int take = L < need - excl ? L : need - excl;
+      const uint32_t bits = (uint32_t)(((e >> 6) << (64 - L)) >> (64 - take));
+      const int o = (e_local + excl) & 31;
+      atomicOr(&s_words[e_local >> 5], bits << (32 - o - take));
+    }
+  }
+  __syncthreads();
+
+  // ---- store the owned words (first bit inside [start, start + agg))
+  const int64_t gw0 = start >> 5;
+  for (int lw = (sh ? 1 : 0) + tid; lw < nwords; lw += HE_THREADS) {
+    const int64_t gw = gw0 + lw;
+    if (gw < a.out_words) a.out[gw] = __byte_perm(s_words[lw], 0, 0x0123);
+    else a.info[2] = 1;
+  }
+}
+
+}  // namespace
+}  // namespace vlz
+
+extern "C" {
+
+size_t vlz_huff_table_bytes(void) { return 65536 * 8 + 65536 * 16; }
+
+int vlz_huff_table(const uint16_t* h_syms, const uint8_t* h_lens, int32_t nsym, void* d_table,
+                   void* stream) {
+  if (!d_table || nsym < 1 || nsym > 65536 || !h_syms || !h_lens) return VLZ_E_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // canonical codewords of the (length, symbol)-sorted book (huffman.py:33-45)
+  std::vector<unsigned long long> staged(2 * (size_t)nsym);
+  unsigned long long code = 0;
+  for (int i = 0; i < nsym; ++i) {
+    const int L = h_lens[i];
+    if (L < 1 || L > vlz::HE_MAXLEN || (i && L < h_lens[i - 1])) return VLZ_E_ARG;
+    staged[2 * i] = h_syms[i];
+    staged[2 * i + 1] = (code << 6) | (unsigned long long)L;
+    code += 1;
+    if (i + 1 < nsym) code <<= (int)h_lens[i + 1] - L;
+  }
+  auto* tab = static_cast<unsigned long long*>(d_table);
+  unsigned long long* dst = tab + 65536;
+  if (cudaMemsetAsync(tab, 0, 65536 * 8, st) != cudaSuccess) return VLZ_E_CUDA;
+  // pageable source: returns once the bytes are staged, `staged` may go
+  if (cudaMemcpyAsync(dst, staged.data(), staged.size() * 8, cudaMemcpyHostToDevice, st) !=
+      cudaSuccess)
+    return VLZ_E_CUDA;
+  vlz::he_table_kernel<<<(nsym + 255) / 256, 256, 0, st>>>(dst, nsym, tab);
+  vlz::g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError() == cudaSuccess ? VLZ_OK : VLZ_E_CUDA;
+}
+
+size_t vlz_huff_encode_ws_size(int64_t n) {
+  const int64_t nchunks = n > 0 ? (n + vlz::HE_CH - 1) / vlz::HE_CH : 1;
+  return 256 + (size_t)nchunks * 8;
+}
+
+int vlz_huff_encode_device(const uint16_t* d_codes, int64_t n, const void* d_table,
+                           int32_t nsym_span, uint8_t* d_out, int64_t out_cap, int64_t* d_info,
+                           void* d_ws, size_t ws_bytes, void* stream) {
+  if (n < 0 || !d_table || !d_info || !d_ws || (n > 0 && (!d_codes || !d_out))) return VLZ_E_ARG;
+  if ((reinterpret_cast<uintptr_t>(d_codes) & 15) || (reinterpret_cast<uintptr_t>(d_out) & 3))
+    return VLZ_E_ARG;
+  if (ws_bytes < vlz_huff_encode_ws_size(n)) return VLZ_E_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t nchunks = n > 0 ? (n + vlz::HE_CH - 1) / vlz::HE_CH : 1;
+  auto* ticket = static_cast<unsigned int*>(d_ws);
+  auto* lb = reinterpret_cast<unsigned long long*>(static_cast<char*>(d_ws) + 256);
+  int64_t ig = (nchunks + 255) / 256;
+  if (ig > 1024) ig = 1024;
+  vlz::he_init_kernel<<<(unsigned)ig, 256, 0, st>>>(lb, nchunks, ticket,
+                                                     reinterpret_cast<long long*>(d_info));
+  vlz::g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (n == 0) return cudaGetLastError() == cudaSuccess ? VLZ_OK : VLZ_E_CUDA;
+  vlz::HEArgs a{};
+  a.codes = d_codes;
+  a.n = n;
+  a.tab = static_cast<const unsigned long long*>(d_table);
+  a.nsym_span = nsym_span;
+  a.out = reinterpret_cast<uint32_t*>(d_out);
+  a.out_words = out_cap / 4;
+  a.lb = lb;
+  a.ticket = ticket;
+  a.info = reinterpret_cast<long long*>(d_info);
+  vlz::huff_encode_kernel<<<(unsigned)nchunks, vlz::HE_THREADS, 0, st>>>(a);
+  vlz::g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError() == cudaSuccess ? VLZ_OK : VLZ_E_CUDA;
+}
+
+}  // extern "C"

@@ -258,5 +258,49 @@ def histogram_device(codes: torch.Tensor, radius: int = 512, stream=None) -> np.
     return freqs.cpu().numpy().view(np.uint64)
 
 
+def huffman_encode_device(codes: torch.Tensor, symbols: np.ndarray, lengths: np.ndarray,
+                          nbits_hint: int | None = None, stream=None):
+    """MSB-first canonical Huffman packing of a uint16 (int16 storage) CUDA
+    code tensor on the GPU (csrc/k_huffenc.cu); returns (payload bytes,
+    bit_length) exactly as huffman.encode.  `nbits_hint` (sum of frequency x
+    length, known once the book is built) sizes the output exactly."""
+    from .errors import CorruptStreamError
+
+    lib = _lib.load()
+    c = codes.contiguous()
+    n = c.numel()
+    if n == 0:
+        return b"", 0
+    syms = np.ascontiguousarray(symbols, dtype=np.uint16)
+    lens = np.ascontiguousarray(lengths, dtype=np.uint8)
+    maxlen = int(lens.max())
+    if maxlen > 58:
+        raise ValueError("codeword longer than 58 bits")
+    dev = c.device
+    st = _stream(stream)
+    tab = torch.empty(int(lib.vlz_huff_table_bytes()), dtype=torch.uint8, device=dev)
+    rc = lib.vlz_huff_table(syms.ctypes.data, lens.ctypes.data, len(syms), _ptr(tab), st)
+    if rc != 0:
+        raise RuntimeError(f"vlz_huff_table failed ({rc})")
+    bits_cap = int(nbits_hint) if nbits_hint is not None else n * maxlen
+    cap = (bits_cap + 31) // 32 * 4 + 4
+    out = torch.empty(cap, dtype=torch.uint8, device=dev)
+    ws = torch.empty(int(lib.vlz_huff_encode_ws_size(n)), dtype=torch.uint8, device=dev)
+    info = torch.empty(4, dtype=torch.int64, device=dev)
+    rc = lib.vlz_huff_encode_device(_ptr(c), n, _ptr(tab), int(syms.max()) + 1, _ptr(out), cap,
+                                    _ptr(info), _ptr(ws), ws.numel(), st)
+    if rc != 0:
+        raise RuntimeError(f"vlz_huff_encode_device failed ({rc})")
+    inf = info.cpu().tolist()
+    none = (1 << 63) - 1
+    bad = inf[1] if inf[1] != none else inf[3]
+    if bad != none:
+        raise CorruptStreamError(f"symbol {bad & 0xFFFF} not in the codebook")
+    if inf[2]:
+        raise RuntimeError("vlz_huff_encode_device: output capacity too small")
+    nb = int(inf[0])
+    return out[: (nb + 7) // 8].cpu().numpy().tobytes(), nb
+
+
 def launch_count() -> int:
     return int(_lib.load().vlz_launch_count())

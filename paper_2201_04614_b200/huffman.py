@@ -86,7 +86,12 @@ def build_codebook(codes) -> HuffmanCodebook:
 
 
 def encode(codes, codebook: HuffmanCodebook):
-    """Pack a symbol stream into bits; returns (payload bytes, bit_length)."""
+    """Pack a symbol stream into bits; returns (payload bytes, bit_length).
+    A CUDA tensor of uint16 codes is packed on the GPU (csrc/k_huffenc.cu)."""
+    if hasattr(codes, "is_cuda") and codes.is_cuda:
+        from .gpu import huffman_encode_device
+
+        return huffman_encode_device(codes, codebook.symbols, codebook.lengths)
     lib = _lib.load()
     c = np.ascontiguousarray(codes).ravel()
     if c.size == 0:

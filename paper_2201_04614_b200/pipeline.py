@@ -52,10 +52,16 @@ def _compress(data: np.ndarray, config: CompressionConfig, want_stream: bool):
     except BoundTooSmallError as exc:
         raise BoundTooSmallError(exc.index, float(data.ravel()[exc.index]), eb) from None
     n_out = dev.n_outliers
-    freqs = gpu.histogram_device(dev.codes[: desc.element_count], config.radius)
+    dcodes = dev.codes[: desc.element_count]
+    freqs = gpu.histogram_device(dcodes, config.radius)
     codebook = build_codebook_from_freqs(freqs)
-    codes16 = dev.codes[: desc.element_count].cpu().numpy().view(np.uint16)
-    bits, nbits = encode(codes16, codebook)
+    # exact payload size: sum of frequency x codeword length
+    nbits_hint = int((freqs[codebook.symbols] * codebook.lengths.astype(np.uint64)).sum())
+    if int(codebook.lengths.max()) <= 58:
+        bits, nbits = gpu.huffman_encode_device(dcodes, codebook.symbols, codebook.lengths,
+                                                nbits_hint=nbits_hint + 64)
+    else:  # pathological book (> 10^12 symbols): native host packer
+        bits, nbits = encode(dcodes.cpu().numpy().view(np.uint16), codebook)
     outliers = dev.outliers[:n_out].cpu().numpy()
     counts = dev.counts[: grid.block_count].cpu().numpy()
     scalars = dev.scalars.cpu().numpy().astype(np.int64)
@@ -63,6 +69,7 @@ def _compress(data: np.ndarray, config: CompressionConfig, want_stream: bool):
                            counts, outliers, grid.block_count)
     stream = None
     if want_stream:
+        codes16 = dcodes.cpu().numpy().view(np.uint16)
         stream = CodeStream(codes=codes16.astype(np.uint32), outlier_values=outliers,
                             outlier_counts=counts, grid=grid, resolved_abs=eb,
                             radius=config.radius,
