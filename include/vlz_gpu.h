@@ -192,6 +192,16 @@ size_t vlz_huff_encode_ws_size(int64_t n);
 int vlz_huff_encode_device(const uint16_t* d_codes, int64_t n, const void* d_table,
                            int32_t nsym_span, uint8_t* d_out, int64_t out_cap, int64_t* d_info,
                            void* d_ws, size_t ws_bytes, void* stream);
+/* device decode (huffman.py:125-207 on the GPU, csrc/k_huffdec.cu):
+ * self-synchronising parallel decode of the single MSB-first stream.
+ * d_payload: 4-byte aligned device copy of the payload (nbytes).  Returns the
+ * same verdict codes as vlz_huff_decode (0 ok, 1..5) with *h_consumed, or a
+ * negative VLZ_E_*; synchronises `stream`.  Code lengths <= 58. */
+size_t vlz_huff_decode_ws_size(int64_t nbytes);
+int vlz_huff_decode_device(const uint8_t* d_payload, int64_t nbytes, int64_t bit_length,
+                           const uint16_t* h_syms, const uint8_t* h_lens, int32_t nsym,
+                           int64_t count, uint16_t* d_out, int64_t* h_consumed, void* d_ws,
+                           size_t ws_bytes, void* stream);
 /* decode (huffman.py:125-207): exactly `count` symbols; returns 0 or the
  * reference's verdict 1..5 (empty/short payload/underrun/invalid prefix/
  * consumed != declared bits) */

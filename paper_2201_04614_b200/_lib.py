@@ -73,6 +73,9 @@ PROTOTYPES = {
     "vlz_huff_encode_ws_size": (ctypes.c_size_t, [_i64]),
     "vlz_huff_encode_device": (ctypes.c_int, [_vp, _i64, _vp, ctypes.c_int32, _vp, _i64, _vp, _vp,
                                               ctypes.c_size_t, _vp]),
+    "vlz_huff_decode_ws_size": (ctypes.c_size_t, [_i64]),
+    "vlz_huff_decode_device": (ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, ctypes.c_int32, _i64,
+                                              _vp, _P(_i64), _vp, ctypes.c_size_t, _vp]),
     "vlz_huff_decode": (ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, ctypes.c_int32, _i64, _vp,
                                        _P(_i64)]),
     "vlz_launch_count": (_i64, []),

@@ -1,0 +1,451 @@
+// k_huffdec.cu -- canonical Huffman decoding of the VLZ1 code stream on the
+// GPU (the reference's decode, huffman.py:125-207: exactly `count` symbols
+// from one unchunked MSB-first stream, same verdicts).
+//
+// The container stores no index into the bit stream, so the decoder
+// self-synchronises (prefix codes resynchronise within a few codewords):
+//  1. the payload is cut into subsequences of HD_S bits; thread k decodes
+//     every codeword that STARTS inside [k*S, (k+1)*S), beginning at the
+//     guessed boundary k*S -> (start s_k, end e_k, symbols c_k);
+//  2. sync passes: thread k re-decodes from e_{k-1} whenever s_k != e_{k-1};
+//     a pass that changes nothing proves every start lies on the true
+//     codeword chain from bit 0 (after 16 passes one thread walks the chain);
+//  3. exclusive scan of c_k (decoupled look-back) -> output offsets;
+//  4. write pass: re-decode, store symbols with index < count, and settle
+//     the verdict: the first subsequence (in stream order) that reaches
+//     `count` or stops on an error decides it.
+// Decoding: a 2^LB-entry (symbol, length) table in shared memory for
+// codewords up to LB <= 11 bits; longer ones by the canonical first-code
+// test per length (huffman.py:33-45 ordering).  The bit window is a 64-bit
+// register refilled 32 bits at a time from big-endian words.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <vector>
+
+#include "../../include/vlz_gpu.h"
+#include "launch.cuh"
+#include "lookback.cuh"
+
+namespace vlz {
+namespace {
+
+constexpr int HD_S = 1024;        // bits per subsequence
+constexpr int HD_THREADS = 256;
+constexpr int HD_LBMAX = 11;      // table bits
+constexpr int HD_MAXLEN = 58;
+constexpr int HD_SCAN_IPT = 8;
+constexpr int HD_SCAN_CH = 256 * HD_SCAN_IPT;
+
+struct HDMeta {
+  unsigned long long first_code[HD_MAXLEN + 2];
+  unsigned int first_idx[HD_MAXLEN + 2];
+  unsigned int cnt[HD_MAXLEN + 2];
+  unsigned int lut[1 << HD_LBMAX];  // sym << 8 | len (0: longer or invalid)
+  int lb, maxlen;
+};
+
+struct HDArgs {
+  const uint32_t* words;  // payload as 32-bit words (4-byte aligned)
+  int64_t nbytes, total_bits;
+  const HDMeta* meta;
+  const uint16_t* syms;  // canonical order
+  int64_t nsub;
+  long long* s;  // start of subsequence k (on the true chain after sync)
+  long long* e;  // end (error: the reference's `consumed`)
+  int* c;        // symbols
+  int* err;      // 0, 3 underrun, 4 invalid prefix
+  long long* o;  // exclusive offsets (int64)
+  unsigned long long* lb;
+  unsigned int* ticket;
+  unsigned int* changed;
+  long long* verdict;  // [0] deciding k (min), [1] consumed on success
+  int64_t count;
+  uint16_t* out;
+};
+
+__device__ __forceinline__ uint32_t ld_word(const HDArgs& a, int64_t w) {
+  const int64_t nw = (a.nbytes + 3) >> 2;
+  if (w >= nw) return 0u;
+  uint32_t x = a.words[w];
+  if (w == nw - 1 && (a.nbytes & 3)) {
+    const int keep = (int)(a.nbytes & 3);  // bytes in little-endian order
+    x &= (1u << (8 * keep)) - 1u;
+  }
+  return __byte_perm(x, 0, 0x0123);
+}
+
+// up to 64 bits starting at bit p, left-aligned (bits past the payload = 0)
+__device__ __forceinline__ unsigned long long peek64(const HDArgs& a, int64_t p) {
+  const int64_t w = p >> 5;
+  const int off = (int)(p & 31);
+  const unsigned long long hi = ((unsigned long long)ld_word(a, w) << 32) | ld_word(a, w + 1);
+  if (off == 0) return hi;
+  return (hi << off) | ((unsigned long long)ld_word(a, w + 2) >> (32 - off));
+}
+
+// Decode the codewords of subsequence k that start in [start, lim).
+// WRITE: store symbols at out[o + j] for o + j < count.
+template <bool WRITE>
+__device__ void decode_run(const HDArgs& a, const HDMeta& m, int64_t k, long long start,
+                           long long o, long long& end, int& count_out, int& err_out) {
+  const long long lim = (long long)(k + 1) * HD_S;
+  const long long tb = a.total_bits;
+  long long pos = start;
+  int c = 0, err = 0;
+  const int LB = m.lb;
+  // register bit window
+  int64_t wi = pos >> 5;
+  unsigned long long buf = ((unsigned long long)ld_word(a, wi) << 32) | ld_word(a, wi + 1);
+  buf <<= (int)(pos & 31);
+  int nb = 64 - (int)(pos & 31);
+  wi += 2;
+  while (pos < lim && pos < tb) {
+    if (WRITE && o + c >= a.count) break;
+    if (nb < 32) {
+      buf |= (unsigned long long)ld_word(a, wi) << (32 - nb);
+      ++wi;
+      nb += 32;
+    }
+    const unsigned int ent = m.lut[(unsigned)(buf >> (64 - LB))];
+    int len = (int)(ent & 0xffu);
+    unsigned sym;
+    if (len) {
+      sym = ent >> 8;
+    } else {
+      // canonical test for lengths LB+1 .. maxlen
+      const unsigned long long win = peek64(a, pos);
+      len = 0;
+      for (int l = LB + 1; l <= m.maxlen; ++l) {
+        const unsigned long long code = win >> (64 - l);
+        if (code >= m.first_code[l] && code - m.first_code[l] < m.cnt[l]) {
+          len = l;
+          sym = a.syms[m.first_idx[l] + (unsigned)(code - m.first_code[l])];
+          break;
+        }
+      }
+      if (len == 0) {  // no codeword: invalid prefix if maxlen+1 bits exist
+        if (tb - pos >= (long long)m.maxlen + 1) {
+          err = 4;
+          pos += m.maxlen + 1;
+        } else {
+          err = 3;
+          pos = tb;
+        }
+        break;
+      }
+    }
+    if (pos + len > tb) {  // the stream runs out mid-codeword
+      err = 3;
+      pos = tb;
+      break;
+    }
+    if (WRITE) {
+      const long long idx = o + c;
+      a.out[idx] = (uint16_t)sym;
+      if (idx == a.count - 1) a.verdict[1] = pos + len;
+    }
+    pos += len;
+    ++c;
+    if (len < nb) {
+      buf <<= len;
+      nb -= len;
+    } else {  // long codeword: reload the window at the new position
+      wi = pos >> 5;
+      buf = ((unsigned long long)ld_word(a, wi) << 32) | ld_word(a, wi + 1);
+      buf <<= (int)(pos & 31);
+      nb = 64 - (int)(pos & 31);
+      wi += 2;
+    }
+  }
+  end = pos;
+  count_out = c;
+  err_out = err;
+}
+
+__device__ __forceinline__ void load_meta(const HDArgs& a, HDMeta& sm) {
+  const int words = (int)(sizeof(HDMeta) / 4);
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(a.meta);
+  uint32_t* dst = reinterpret_cast<uint32_t*>(&sm);
+  for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
+  __syncthreads();
+}
+
+// MODE 0: first pass from the guessed boundaries; 1: sync pass
+template <int MODE>
+__global__ void __launch_bounds__(HD_THREADS) hd_pass_kernel(HDArgs a) {
+  __shared__ HDMeta sm;
+  load_meta(a, sm);
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= a.nsub) return;
+  long long start;
+  if (MODE == 0) {
+    start = (long long)k * HD_S;
+  } else {
+    if (k == 0) return;
+    volatile int* verr = a.err;
+    volatile long long* ve = a.e;
+    if (verr[k - 1]) return;  // chain stops there (or it is not settled yet)
+    start = ve[k - 1];
+    if (start == a.s[k]) return;
+  }
+  long long end;
+  int c, err;
+  decode_run<false>(a, sm, k, start, 0, end, c, err);
+  a.s[k] = start;
+  a.c[k] = c;
+  a.err[k] = err;
+  __threadfence();
+  reinterpret_cast<volatile long long*>(a.e)[k] = end;
+  if (MODE == 1) atomicAdd(a.changed, 1u);
+}
+
+// fallback after many passes: one thread walks the chain in order
+__global__ void hd_chain_kernel(HDArgs a) {
+  __shared__ HDMeta sm;
+  load_meta(a, sm);
+  if (threadIdx.x != 0) return;
+  for (int64_t k = 1; k < a.nsub; ++k) {
+    if (a.err[k - 1]) break;
+    const long long start = a.e[k - 1];
+    if (start == a.s[k]) continue;
+    long long end;
+    int c, err;
+    decode_run<false>(a, sm, k, start, 0, end, c, err);
+    a.s[k] = start;
+    a.e[k] = end;
+    a.c[k] = c;
+    a.err[k] = err;
+  }
+}
+
+__global__ void hd_init_kernel(HDArgs a, int64_t nchunks) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0) {
+    *a.ticket = 0;
+    *a.changed = 0;
+    a.verdict[0] = 0x7fffffffffffffffll;
+    a.verdict[1] = -1;
+  }
+  for (int64_t k = i; k < nchunks; k += (int64_t)gridDim.x * blockDim.x) a.lb[k] = 0;
+}
+
+// exclusive scan of c_k -> o_k
+__global__ void __launch_bounds__(256) hd_scan_kernel(HDArgs a) {
+  __shared__ long long s_warp[8];
+  __shared__ long long s_excl;
+  __shared__ unsigned int s_tile;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) s_tile = atomicAdd(a.ticket, 1u);
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const int64_t base = tile * HD_SCAN_CH + (int64_t)tid * HD_SCAN_IPT;
+  long long v[HD_SCAN_IPT];
+  long long tsum = 0;
+#pragma unroll
+  for (int j = 0; j < HD_SCAN_IPT; ++j) {
+    v[j] = (base + j < a.nsub) ? a.c[base + j] : 0;
+    tsum += v[j];
+  }
+  long long inc = tsum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long u = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += u;
+  }
+  if (lane == 31) s_warp[wid] = inc;
+  __syncthreads();
+  long long wbase = 0, agg = 0;
+  for (int w = 0; w < 8; ++w) {
+    if (w < wid) wbase += s_warp[w];
+    agg += s_warp[w];
+  }
+  if (wid == 0) {
+    const long long ex = lookback_exclusive(a.lb, tile, agg, lane);
+    if (lane == 0) s_excl = ex;
+  }
+  __syncthreads();
+  long long run = s_excl + wbase + inc - tsum;
+#pragma unroll
+  for (int j = 0; j < HD_SCAN_IPT; ++j) {
+    if (base + j < a.nsub) a.o[base + j] = run;
+    run += v[j];
+  }
+}
+
+__global__ void __launch_bounds__(HD_THREADS) hd_write_kernel(HDArgs a) {
+  __shared__ HDMeta sm;
+  load_meta(a, sm);
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= a.nsub) return;
+  const long long o = a.o[k];
+  const int c = a.c[k];
+  // deciding subsequence: reaches `count`, or stops on an error first
+  if (o + c >= a.count || a.err[k]) atomicMin(a.verdict, (long long)k);
+  if (o >= a.count) return;
+  long long end;
+  int cc, err;
+  decode_run<true>(a, sm, k, a.s[k], o, end, cc, err);
+}
+
+}  // namespace
+}  // namespace vlz
+
+extern "C" {
+
+size_t vlz_huff_decode_ws_size(int64_t nbytes) {
+  const int64_t bits = nbytes * 8;
+  const int64_t nsub = bits > 0 ? (bits + vlz::HD_S - 1) / vlz::HD_S : 1;
+  const int64_t nchunks = (nsub + vlz::HD_SCAN_CH - 1) / vlz::HD_SCAN_CH;
+  size_t b = 256;                                         // counters + verdict
+  b += (sizeof(vlz::HDMeta) + 255) / 256 * 256;           // tables
+  b += 65536 * 2;                                         // canonical symbols
+  b += ((size_t)nsub * (8 + 8 + 4 + 4 + 8) + 255) / 256 * 256;
+  b += (size_t)nchunks * 8 + 256;
+  return b;
+}
+
+// Returns the reference's verdict (0 ok, 1..5 as vlz_huff_decode) or a
+// negative error; synchronises `stream` (the sync passes need the host).
+int vlz_huff_decode_device(const uint8_t* d_payload, int64_t nbytes, int64_t bit_length,
+                           const uint16_t* h_syms, const uint8_t* h_lens, int32_t nsym,
+                           int64_t count, uint16_t* d_out, int64_t* h_consumed, void* d_ws,
+                           size_t ws_bytes, void* stream) {
+  if (!h_consumed || nbytes < 0 || count < 0 || nsym < 1 || !h_syms || !h_lens) return VLZ_E_ARG;
+  *h_consumed = 0;
+  if (count == 0) return bit_length != 0 ? 1 : 0;  // huffman.py order
+  if (nbytes * 8 < bit_length) return 2;
+  if (!d_out || !d_ws || (nbytes > 0 && !d_payload) ||
+      (reinterpret_cast<uintptr_t>(d_payload) & 3) || ws_bytes < vlz_huff_decode_ws_size(nbytes))
+    return VLZ_E_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+
+  // ---- tables (canonical order, huffman.py:33-45)
+  vlz::HDMeta meta;
+  std::memset(&meta, 0, sizeof(meta));
+  int maxlen = 0;
+  for (int i = 0; i < nsym; ++i) {
+    if (h_lens[i] < 1 || (i && h_lens[i] < h_lens[i - 1])) return VLZ_E_ARG;
+    maxlen = h_lens[i] > maxlen ? h_lens[i] : maxlen;
+  }
+  if (maxlen > vlz::HD_MAXLEN) return VLZ_E_ARG;
+  for (int i = 0; i < nsym; ++i) meta.cnt[h_lens[i]] += 1;
+  {
+    unsigned long long code = 0;
+    unsigned idx = 0;
+    for (int l = 1; l <= maxlen; ++l) {
+      meta.first_code[l] = code;
+      meta.first_idx[l] = idx;
+      code = (code + meta.cnt[l]) << 1;
+      idx += meta.cnt[l];
+    }
+  }
+  const int lb = maxlen < vlz::HD_LBMAX ? maxlen : vlz::HD_LBMAX;
+  meta.lb = lb;
+  meta.maxlen = maxlen;
+  {
+    unsigned long long code = 0;
+    for (int i = 0; i < nsym; ++i) {
+      const int L = h_lens[i];
+      if (L <= lb) {
+        const unsigned long long b0 = code << (lb - L);
+        const unsigned long long span = 1ull << (lb - L);
+        for (unsigned long long t = 0; t < span; ++t)
+          meta.lut[b0 + t] = ((unsigned)h_syms[i] << 8) | (unsigned)L;
+      }
+      code += 1;
+      if (i + 1 < nsym) code <<= (int)h_lens[i + 1] - L;
+    }
+  }
+
+  // ---- workspace
+  const int64_t bits = nbytes * 8;
+  const int64_t nsub = bits > 0 ? (bits + vlz::HD_S - 1) / vlz::HD_S : 1;
+  const int64_t nchunks = (nsub + vlz::HD_SCAN_CH - 1) / vlz::HD_SCAN_CH;
+  char* p = static_cast<char*>(d_ws);
+  vlz::HDArgs a{};
+  a.ticket = reinterpret_cast<unsigned int*>(p);
+  a.changed = reinterpret_cast<unsigned int*>(p + 8);
+  a.verdict = reinterpret_cast<long long*>(p + 16);
+  size_t off = 256;
+  auto* dmeta = reinterpret_cast<vlz::HDMeta*>(p + off);
+  off += (sizeof(vlz::HDMeta) + 255) / 256 * 256;
+  auto* dsyms = reinterpret_cast<uint16_t*>(p + off);
+  off += 65536 * 2;
+  a.s = reinterpret_cast<long long*>(p + off);
+  a.e = a.s + nsub;
+  a.o = a.e + nsub;
+  a.c = reinterpret_cast<int*>(a.o + nsub);
+  a.err = a.c + nsub;
+  off += ((size_t)nsub * 32 + 255) / 256 * 256;
+  a.lb = reinterpret_cast<unsigned long long*>(p + off);
+  a.words = reinterpret_cast<const uint32_t*>(d_payload);
+  a.nbytes = nbytes;
+  a.total_bits = bits;
+  a.meta = dmeta;
+  a.syms = dsyms;
+  a.nsub = nsub;
+  a.count = count;
+  a.out = d_out;
+
+  auto ok = [](cudaError_t e) { return e == cudaSuccess; };
+  if (!ok(cudaMemcpyAsync(dmeta, &meta, sizeof(meta), cudaMemcpyHostToDevice, st)) ||
+      !ok(cudaMemcpyAsync(dsyms, h_syms, (size_t)nsym * 2, cudaMemcpyHostToDevice, st)))
+    return VLZ_E_CUDA;
+  int64_t ig = (nchunks + 255) / 256;
+  if (ig < 1) ig = 1;
+  if (ig > 1024) ig = 1024;
+  vlz::hd_init_kernel<<<(unsigned)ig, 256, 0, st>>>(a, nchunks);
+  const unsigned grid = (unsigned)((nsub + vlz::HD_THREADS - 1) / vlz::HD_THREADS);
+  vlz::hd_pass_kernel<0><<<grid, vlz::HD_THREADS, 0, st>>>(a);
+  vlz::g_launches.fetch_add(2, std::memory_order_relaxed);
+  // ---- sync passes until nothing changes
+  bool settled = nsub == 1;
+  for (int it = 0; it < 16 && !settled; ++it) {
+    if (!ok(cudaMemsetAsync(a.changed, 0, 4, st))) return VLZ_E_CUDA;
+    vlz::hd_pass_kernel<1><<<grid, vlz::HD_THREADS, 0, st>>>(a);
+    vlz::g_launches.fetch_add(1, std::memory_order_relaxed);
+    unsigned int changed = 0;
+    if (!ok(cudaMemcpyAsync(&changed, a.changed, 4, cudaMemcpyDeviceToHost, st)) ||
+        !ok(cudaStreamSynchronize(st)))
+      return VLZ_E_CUDA;
+    settled = changed == 0;
+  }
+  if (!settled) {
+    vlz::hd_chain_kernel<<<1, 32, 0, st>>>(a);
+    vlz::g_launches.fetch_add(1, std::memory_order_relaxed);
+  }
+  vlz::hd_scan_kernel<<<(unsigned)nchunks, 256, 0, st>>>(a);
+  vlz::hd_write_kernel<<<grid, vlz::HD_THREADS, 0, st>>>(a);
+  vlz::g_launches.fetch_add(2, std::memory_order_relaxed);
+  if (!ok(cudaGetLastError())) return VLZ_E_CUDA;
+
+  // ---- verdict
+  long long v[2];
+  if (!ok(cudaMemcpyAsync(v, a.verdict, 16, cudaMemcpyDeviceToHost, st)) ||
+      !ok(cudaStreamSynchronize(st)))
+    return VLZ_E_CUDA;
+  const long long kd = v[0];
+  if (kd == 0x7fffffffffffffffll) {  // chain ended at the payload end, count not reached
+    *h_consumed = bits;
+    return 3;
+  }
+  long long ok_k[3];  // o, c, err of the deciding subsequence
+  long long ek;
+  int ci[2];
+  if (!ok(cudaMemcpyAsync(&ok_k[0], a.o + kd, 8, cudaMemcpyDeviceToHost, st)) ||
+      !ok(cudaMemcpyAsync(&ci[0], a.c + kd, 4, cudaMemcpyDeviceToHost, st)) ||
+      !ok(cudaMemcpyAsync(&ci[1], a.err + kd, 4, cudaMemcpyDeviceToHost, st)) ||
+      !ok(cudaMemcpyAsync(&ek, a.e + kd, 8, cudaMemcpyDeviceToHost, st)) ||
+      !ok(cudaStreamSynchronize(st)))
+    return VLZ_E_CUDA;
+  if (ok_k[0] + ci[0] >= count) {  // count reached before any error
+    *h_consumed = v[1];
+    return v[1] != bit_length ? 5 : 0;
+  }
+  *h_consumed = ek;  // error position (the reference's `consumed`)
+  return ci[1];
+}
+
+}  // extern "C"

@@ -117,17 +117,8 @@ def encode(codes, codebook: HuffmanCodebook):
     return out[: (nb + 7) // 8].tobytes(), nb
 
 
-def decode(payload: bytes, bit_length: int, codebook: HuffmanCodebook, count: int) -> np.ndarray:
-    """Decode exactly `count` symbols consuming exactly `bit_length` bits."""
-    lib = _lib.load()
-    out = np.empty(max(int(count), 1), dtype=np.uint16)
-    buf = np.frombuffer(payload, dtype=np.uint8) if len(payload) else np.zeros(1, np.uint8)
-    syms = codebook.symbols.astype(np.uint16)
-    lens = np.ascontiguousarray(codebook.lengths, dtype=np.uint8)
-    consumed = ctypes.c_int64(0)
-    rc = lib.vlz_huff_decode(buf.ctypes.data, len(payload), int(bit_length), syms.ctypes.data,
-                             lens.ctypes.data, len(syms), int(count), out.ctypes.data,
-                             ctypes.byref(consumed))
+def raise_decode_verdict(rc: int, consumed: int, bit_length: int) -> None:
+    """The reference's decode errors (huffman.py:135-207), by verdict code."""
     if rc == 1:
         raise CorruptStreamError("nonzero bit length for an empty stream")
     if rc == 2:
@@ -137,6 +128,49 @@ def decode(payload: bytes, bit_length: int, codebook: HuffmanCodebook, count: in
     if rc == 4:
         raise CorruptStreamError("invalid prefix in bit stream")
     if rc == 5:
-        raise CorruptStreamError(
-            f"decoded {consumed.value} bits but the stream declares {bit_length}")
+        raise CorruptStreamError(f"decoded {consumed} bits but the stream declares {bit_length}")
+    if rc != 0:
+        raise RuntimeError(f"Huffman decode failed ({rc})")
+
+
+def decode(payload: bytes, bit_length: int, codebook: HuffmanCodebook, count: int) -> np.ndarray:
+    """Decode exactly `count` symbols consuming exactly `bit_length` bits
+    (native host decoder; decode_device runs on the GPU)."""
+    lib = _lib.load()
+    out = np.empty(max(int(count), 1), dtype=np.uint16)
+    buf = np.frombuffer(payload, dtype=np.uint8) if len(payload) else np.zeros(1, np.uint8)
+    syms = codebook.symbols.astype(np.uint16)
+    lens = np.ascontiguousarray(codebook.lengths, dtype=np.uint8)
+    consumed = ctypes.c_int64(0)
+    rc = lib.vlz_huff_decode(buf.ctypes.data, len(payload), int(bit_length), syms.ctypes.data,
+                             lens.ctypes.data, len(syms), int(count), out.ctypes.data,
+                             ctypes.byref(consumed))
+    raise_decode_verdict(rc, consumed.value, bit_length)
+    return out[: int(count)]
+
+
+def decode_device(payload: bytes, bit_length: int, codebook: HuffmanCodebook, count: int,
+                  device=None):
+    """decode() on the GPU (csrc/k_huffdec.cu, self-synchronising parallel
+    decode); returns an int16-storage CUDA tensor of `count` uint16 symbols."""
+    import torch
+
+    from .gpu import _stream
+
+    lib = _lib.load()
+    dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    nbytes = len(payload)
+    dpay = torch.zeros((nbytes + 3) // 4 * 4 + 16, dtype=torch.uint8, device=dev)
+    if nbytes:
+        dpay[:nbytes].copy_(torch.frombuffer(bytearray(payload), dtype=torch.uint8))
+    out = torch.empty(max(int(count), 1), dtype=torch.int16, device=dev)
+    ws = torch.empty(int(lib.vlz_huff_decode_ws_size(nbytes)), dtype=torch.uint8, device=dev)
+    syms = np.ascontiguousarray(codebook.symbols, dtype=np.uint16)
+    lens = np.ascontiguousarray(codebook.lengths, dtype=np.uint8)
+    consumed = ctypes.c_int64(0)
+    rc = lib.vlz_huff_decode_device(dpay.data_ptr(), nbytes, int(bit_length), syms.ctypes.data,
+                                    lens.ctypes.data, len(syms), int(count), out.data_ptr(),
+                                    ctypes.byref(consumed), ws.data_ptr(), ws.numel(),
+                                    _stream(None))
+    raise_decode_verdict(rc, consumed.value, bit_length)
     return out[: int(count)]

@@ -19,7 +19,7 @@ import torch
 from . import gpu
 from .container import ParsedContainer, deserialize, serialize_parts
 from .errors import BoundTooSmallError, ConfigError
-from .huffman import build_codebook_from_freqs, decode, encode
+from .huffman import build_codebook_from_freqs, decode, decode_device, encode
 from .model import (
     ArrayDescriptor,
     CodeStream,
@@ -88,12 +88,16 @@ def compress_detailed(data: np.ndarray, config: CompressionConfig):
 
 
 def decompress_parsed(parsed: ParsedContainer, thread_count: int = 1):
-    """reconstruct.py:74-124: Huffman decode, then the GPU block reconstruction
-    (thread_count is accepted for compatibility and ignored)."""
+    """reconstruct.py:74-124: Huffman decode and block reconstruction, both on
+    the GPU (thread_count is accepted for compatibility and ignored)."""
     desc = parsed.descriptor
     grid = build_block_grid(desc, parsed.block_edge)
-    codes = decode(parsed.code_bits, parsed.code_bit_length, parsed.codebook,
-                   desc.element_count)
+    cb = parsed.codebook
+    if len(cb.lengths) and int(cb.lengths.max()) <= 58:
+        codes = decode_device(parsed.code_bits, parsed.code_bit_length, cb, desc.element_count,
+                              device=_device())
+    else:  # empty or pathological book: verdicts from the native host decoder
+        codes = decode(parsed.code_bits, parsed.code_bit_length, cb, desc.element_count)
     out = reconstruct_arrays(codes, parsed.outlier_values, parsed.outlier_counts,
                              parsed.padding_values, grid, parsed.resolved_abs, parsed.radius,
                              parsed.padding_policy)

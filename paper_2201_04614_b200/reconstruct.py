@@ -23,11 +23,14 @@ def reconstruct_arrays(codes: np.ndarray, outlier_values: np.ndarray, outlier_co
     if not torch.cuda.is_available():
         raise RuntimeError("paper_2201_04614_b200 needs a CUDA device (B200); no CPU fallback")
     dev = torch.device("cuda", torch.cuda.current_device())
-    codes = np.ascontiguousarray(codes)
-    if codes.dtype == np.uint16:
-        c = torch.from_numpy(codes.view(np.int16)).to(dev)
+    if isinstance(codes, torch.Tensor):  # already on the device (GPU Huffman decode)
+        c = codes.to(dev)
     else:
-        c = torch.from_numpy(codes.astype(np.uint32, copy=False).view(np.int32)).to(dev)
+        codes = np.ascontiguousarray(codes)
+        if codes.dtype == np.uint16:
+            c = torch.from_numpy(codes.view(np.int16)).to(dev)
+        else:
+            c = torch.from_numpy(codes.astype(np.uint32, copy=False).view(np.int32)).to(dev)
     ov = torch.from_numpy(np.ascontiguousarray(outlier_values, dtype=np.float32)).to(dev)
     cnt = torch.from_numpy(np.ascontiguousarray(outlier_counts, dtype=np.int64)).to(dev)
     sc = torch.from_numpy(np.ascontiguousarray(scalars, dtype=np.int64)).to(dev)

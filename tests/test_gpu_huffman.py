@@ -80,3 +80,112 @@ def test_error_precedence():
         s = np.array(stream * 3000, np.uint16)
         with pytest.raises(CorruptStreamError, match=f"symbol {bad} not in the codebook"):
             gpu.huffman_encode_device(_dev(s), cb.symbols, cb.lengths)
+
+
+# ---- decoder (csrc/k_huffdec.cu) -------------------------------------------
+
+from conftest import load_json  # noqa: E402
+
+from paper_2201_04614_b200 import errors as E  # noqa: E402
+from paper_2201_04614_b200.container import deserialize  # noqa: E402
+from paper_2201_04614_b200.huffman import HuffmanCodebook, decode, decode_device  # noqa: E402
+
+
+def _verdict(fn):
+    try:
+        r = fn()
+        return ("ok", r if isinstance(r, np.ndarray) else r.cpu().numpy().view(np.uint16))
+    except E.VlzError as exc:
+        return (type(exc).__name__, str(exc))
+
+
+def _same_verdict(payload, nbits, cb, count):
+    h = _verdict(lambda: decode(payload, nbits, cb, count))
+    d = _verdict(lambda: decode_device(payload, nbits, cb, count))
+    assert h[0] == d[0]
+    if h[0] == "ok":
+        assert np.array_equal(h[1], d[1])
+    else:
+        assert h[1] == d[1]
+    return h
+
+
+@pytest.mark.parametrize("n", [1, 2, 31, 280, 281, 4096, 100_003, 3_000_000])
+def test_decode_round_trip(n):
+    rng = np.random.default_rng(n + 1)
+    codes = (512 + np.round(rng.normal(0, 4, n))).astype(np.uint16)
+    codes[rng.integers(0, n, max(1, n // 40))] = 0
+    cb = build_codebook(codes)
+    payload, nbits = encode(codes, cb)
+    got = decode_device(payload, nbits, cb, n).cpu().numpy().view(np.uint16)
+    assert np.array_equal(got, codes)
+
+
+def test_decode_deep_and_skewed_books():
+    rng = np.random.default_rng(5)
+    fib = [1, 1]
+    while len(fib) < 32:
+        fib.append(fib[-1] + fib[-2])
+    codes = np.concatenate([np.full(f, 40 + k, np.uint16) for k, f in enumerate(fib)])
+    rng.shuffle(codes)
+    for c in (codes[:500_000], np.full(5000, 9, np.uint16),
+              rng.choice(np.arange(1, 2001, dtype=np.uint16), 400_000,
+                         p=rng.dirichlet(np.full(2000, 0.2))).astype(np.uint16)):
+        cb = build_codebook(c)
+        payload, nbits = encode(c, cb)
+        got = decode_device(payload, nbits, cb, c.size).cpu().numpy().view(np.uint16)
+        assert np.array_equal(got, c)
+
+
+def test_decode_verdicts_match_host():
+    rng = np.random.default_rng(9)
+    codes = (300 + np.round(rng.normal(0, 3, 50_000))).astype(np.uint16)
+    cb = build_codebook(codes)
+    payload, nbits = encode(codes, cb)
+    n = codes.size
+    cases = [
+        (payload, nbits, n - 1),            # fewer symbols than the stream holds -> 5
+        (payload, nbits, n + 7),            # more symbols than the stream holds -> 3
+        (payload, nbits + 3, n),            # declared length too long -> 5 or 2
+        (payload, nbits - 1, n),            # declared length too short -> 5
+        (payload[: len(payload) // 2], nbits // 2, n),  # truncated -> 3
+        (payload, 0, 0),                    # empty stream, zero bits -> ok
+        (payload, 5, 0),                    # empty stream, nonzero bits -> 1
+        (payload[:10], nbits, n),           # shorter than declared -> 2
+        (b"", 0, 3),                        # nothing to read -> 3
+    ]
+    for pl, nb, cnt in cases:
+        _same_verdict(pl, nb, cb, cnt)
+    # incomplete book (one symbol, code "0"): any 1 bit is an invalid prefix
+    one = HuffmanCodebook.from_lengths(np.array([7], np.uint32), np.array([1], np.uint8))
+    for pl, nb, cnt in ((b"\x00\x10", 16, 16), (b"\x00" * 300 + b"\x80", 2408, 2408),
+                        (b"\x00" * 300, 2400, 2400)):
+        _same_verdict(pl, nb, one, cnt)
+    # random corruption of a valid payload
+    for t in range(20):
+        pl = bytearray(payload)
+        for _ in range(1 + t % 4):
+            i = int(rng.integers(0, len(pl)))
+            pl[i] ^= 1 << int(rng.integers(0, 8))
+        _same_verdict(bytes(pl), nbits, cb, n)
+
+
+def test_decode_reference_mutated_containers():
+    cases = load_json("container.json")
+    n = 0
+    for c in cases:
+        try:
+            p = deserialize(bytes.fromhex(c["blob"]))
+        except E.VlzError:
+            continue
+        if not len(p.codebook.lengths) or int(p.codebook.lengths.max()) > 58:
+            continue
+        got = _verdict(lambda: decode_device(p.code_bits, p.code_bit_length, p.codebook,
+                                             p.descriptor.element_count))
+        exp = c["expect"]
+        if exp is None:
+            assert got[0] == "ok", c["tag"]
+        else:
+            assert got == (exp["type"], exp["message"]), c["tag"]
+        n += 1
+    assert n > 20
