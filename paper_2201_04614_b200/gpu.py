@@ -259,7 +259,8 @@ def histogram_device(codes: torch.Tensor, radius: int = 512, stream=None) -> np.
 
 
 def huffman_encode_device(codes: torch.Tensor, symbols: np.ndarray, lengths: np.ndarray,
-                          nbits_hint: int | None = None, stream=None):
+                          nbits_hint: int | None = None, stream=None,
+                          keep_on_device: bool = False):
     """MSB-first canonical Huffman packing of a uint16 (int16 storage) CUDA
     code tensor on the GPU (csrc/k_huffenc.cu); returns (payload bytes,
     bit_length) exactly as huffman.encode.  `nbits_hint` (sum of frequency x
@@ -299,6 +300,8 @@ def huffman_encode_device(codes: torch.Tensor, symbols: np.ndarray, lengths: np.
     if inf[2]:
         raise RuntimeError("vlz_huff_encode_device: output capacity too small")
     nb = int(inf[0])
+    if keep_on_device:  # (CUDA uint8 tensor, bits): serialize_parts copies it once
+        return out, nb
     return out[: (nb + 7) // 8].cpu().numpy().tobytes(), nb
 
 

@@ -13,6 +13,7 @@ codes are device resident.
 from __future__ import annotations
 
 import ctypes
+import warnings
 from dataclasses import dataclass
 
 import numpy as np
@@ -162,7 +163,10 @@ def decode_device(payload: bytes, bit_length: int, codebook: HuffmanCodebook, co
     nbytes = len(payload)
     dpay = torch.zeros((nbytes + 3) // 4 * 4 + 16, dtype=torch.uint8, device=dev)
     if nbytes:
-        dpay[:nbytes].copy_(torch.frombuffer(bytearray(payload), dtype=torch.uint8))
+        with warnings.catch_warnings():  # read-only view: only ever read (H2D source)
+            warnings.simplefilter("ignore", UserWarning)
+            host = torch.frombuffer(payload, dtype=torch.uint8, count=nbytes)
+        dpay[:nbytes].copy_(host)
     out = torch.empty(max(int(count), 1), dtype=torch.int16, device=dev)
     ws = torch.empty(int(lib.vlz_huff_decode_ws_size(nbytes)), dtype=torch.uint8, device=dev)
     syms = np.ascontiguousarray(codebook.symbols, dtype=np.uint16)

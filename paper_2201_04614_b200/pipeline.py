@@ -59,7 +59,7 @@ def _compress(data: np.ndarray, config: CompressionConfig, want_stream: bool):
     nbits_hint = int((freqs[codebook.symbols] * codebook.lengths.astype(np.uint64)).sum())
     if int(codebook.lengths.max()) <= 58:
         bits, nbits = gpu.huffman_encode_device(dcodes, codebook.symbols, codebook.lengths,
-                                                nbits_hint=nbits_hint + 64)
+                                                nbits_hint=nbits_hint, keep_on_device=True)
     else:  # pathological book (> 10^12 symbols): native host packer
         bits, nbits = encode(dcodes.cpu().numpy().view(np.uint16), codebook)
     outliers = dev.outliers[:n_out].cpu().numpy()

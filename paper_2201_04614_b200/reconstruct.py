@@ -35,7 +35,11 @@ def reconstruct_arrays(codes: np.ndarray, outlier_values: np.ndarray, outlier_co
     cnt = torch.from_numpy(np.ascontiguousarray(outlier_counts, dtype=np.int64)).to(dev)
     sc = torch.from_numpy(np.ascontiguousarray(scalars, dtype=np.int64)).to(dev)
     out = gpu.decompress_device(c, ov, ov.numel(), cnt, sc, grid, eb, radius, padding)
-    return out.cpu().numpy()
+    # one DMA copy into pinned host memory (torch's caching host allocator
+    # recycles it across calls); the array keeps the pinned block alive
+    host = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
+    host.copy_(out)
+    return host.numpy()
 
 
 def reconstruct_stream(stream: CodeStream) -> np.ndarray:
