@@ -184,13 +184,14 @@ int vlz_huff_encode(const uint16_t* h_codes, int64_t n, const uint16_t* h_syms,
  * the end are zero) and fills d_info (int64[4], device): [0] bit length,
  * [1] (index << 16 | symbol) of the first symbol >= nsym_span (= largest book
  * symbol + 1) or INT64_MAX, [2] 1 if out_cap was too small, [3] first symbol
- * absent from the book or INT64_MAX.  Stream-ordered, no host sync. */
+ * absent from the book or INT64_MAX.  max_len = longest book codeword (sizes
+ * shared memory).  Stream-ordered, no host sync. */
 size_t vlz_huff_table_bytes(void);
 int vlz_huff_table(const uint16_t* h_syms, const uint8_t* h_lens, int32_t nsym, void* d_table,
                    void* stream);
 size_t vlz_huff_encode_ws_size(int64_t n);
 int vlz_huff_encode_device(const uint16_t* d_codes, int64_t n, const void* d_table,
-                           int32_t nsym_span, uint8_t* d_out, int64_t out_cap, int64_t* d_info,
+                           int32_t nsym_span, int32_t max_len, uint8_t* d_out, int64_t out_cap, int64_t* d_info,
                            void* d_ws, size_t ws_bytes, void* stream);
 /* device decode (huffman.py:125-207 on the GPU, csrc/k_huffdec.cu):
  * self-synchronising parallel decode of the single MSB-first stream.

@@ -71,7 +71,8 @@ PROTOTYPES = {
     "vlz_huff_table_bytes": (ctypes.c_size_t, []),
     "vlz_huff_table": (ctypes.c_int, [_vp, _vp, ctypes.c_int32, _vp, _vp]),
     "vlz_huff_encode_ws_size": (ctypes.c_size_t, [_i64]),
-    "vlz_huff_encode_device": (ctypes.c_int, [_vp, _i64, _vp, ctypes.c_int32, _vp, _i64, _vp, _vp,
+    "vlz_huff_encode_device": (ctypes.c_int, [_vp, _i64, _vp, ctypes.c_int32, ctypes.c_int32,
+                                              _vp, _i64, _vp, _vp,
                                               ctypes.c_size_t, _vp]),
     "vlz_huff_decode_ws_size": (ctypes.c_size_t, [_i64]),
     "vlz_huff_decode_device": (ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, ctypes.c_int32, _i64,

@@ -4,12 +4,14 @@
 //
 // One pass, no memset of the output:
 //  * a chunk of HE_CH symbols per CTA (dynamic ticket order); every thread
-//    looks up the (codeword, length) of its 16 symbols in the device table;
+//    looks up the lengths of its 32 symbols (u8 table) for the scan and the
+//    (codeword, length) entries again when packing (L1-resident tables);
 //  * block scan of the lengths + decoupled look-back (lookback.cuh) give the
 //    chunk's global bit offset;
 //  * the chunk assembles its bits in shared memory, aligned to the global
-//    32-bit word grid (shared atomicOr; each thread flushes a register word
-//    only when it moves to the next word);
+//    32-bit word grid: each thread shifts its codewords into a 64-bit
+//    accumulator and emits whole words (atomicOr only for the words it
+//    shares with its neighbours);
 //  * a chunk OWNS the output words whose first bit lies inside its bit range;
 //    the one word it shares with the next chunk is completed by reading that
 //    chunk's leading symbols (<= 31 bits, every codeword has >= 1 bit), so
@@ -30,16 +32,18 @@ namespace vlz {
 namespace {
 
 constexpr int HE_THREADS = 256;
-constexpr int HE_SPT = 16;                  // symbols per thread
+constexpr int HE_SPT = 32;                  // symbols per thread
 constexpr int HE_CH = HE_THREADS * HE_SPT;  // symbols per chunk
 constexpr int HE_MAXLEN = 58;
-constexpr int HE_WORDS = (HE_CH * HE_MAXLEN + 31) / 32 + 2;
 constexpr long long HE_NONE = 0x7fffffffffffffffll;
+constexpr size_t HE_TAB = 65536 * 8;        // entries
+constexpr size_t HE_LEN = 65536;            // lengths (u8)
 
 struct HEArgs {
   const uint16_t* codes;
   int64_t n;
   const unsigned long long* tab;  // [65536] codeword << 6 | length, 0 = absent
+  const uint8_t* len;             // [65536] length, 0 = absent
   int32_t nsym_span;              // max codebook symbol + 1 (huffman.py:96)
   uint32_t* out;
   int64_t out_words;
@@ -62,13 +66,24 @@ __global__ void he_init_kernel(unsigned long long* lb, int64_t nchunks, unsigned
 }
 
 __global__ void he_table_kernel(const unsigned long long* staged, int32_t nsym,
-                                unsigned long long* tab) {
+                                unsigned long long* tab, uint8_t* len) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < nsym) tab[staged[2 * i]] = staged[2 * i + 1];
+  if (i < nsym) {
+    const unsigned long long e = staged[2 * i + 1];
+    tab[staged[2 * i]] = e;
+    len[staged[2 * i]] = (uint8_t)(e & 63);
+  }
 }
 
-__global__ void __launch_bounds__(HE_THREADS) huff_encode_kernel(HEArgs a) {
-  __shared__ uint32_t s_words[HE_WORDS];
+__device__ __forceinline__ unsigned sym_at(const uint4* pk, int k) {
+  const uint4 v = pk[k >> 3];
+  const int w = (k >> 1) & 3;
+  const unsigned x = w == 0 ? v.x : w == 1 ? v.y : w == 2 ? v.z : v.w;
+  return (k & 1) ? (x >> 16) : (x & 0xffffu);
+}
+
+__global__ void __launch_bounds__(HE_THREADS, 3) huff_encode_kernel(HEArgs a) {
+  extern __shared__ uint32_t s_words[];  // sized for HE_CH * max_len bits
   __shared__ int s_warp[HE_THREADS / 32];
   __shared__ long long s_start;
   __shared__ unsigned int s_tile;
@@ -79,35 +94,41 @@ __global__ void __launch_bounds__(HE_THREADS) huff_encode_kernel(HEArgs a) {
   const int64_t tile = s_tile;
   const int64_t base = tile * HE_CH;
   const int64_t i0 = base + (int64_t)tid * HE_SPT;
+  const bool full = i0 + HE_SPT <= a.n;
 
-  // ---- symbols -> (codeword, length)
-  unsigned sym[HE_SPT];
-  if (i0 + HE_SPT <= a.n) {
+  // ---- symbols (packed, 16 B vectors) and the next chunk's leading symbols
+  uint4 pk[HE_SPT / 8];
+  if (full) {
     const uint4* v = reinterpret_cast<const uint4*>(a.codes + i0);
-    const uint4 w0 = v[0], w1 = v[1];
-    const unsigned ws[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      sym[2 * k] = ws[k] & 0xffffu;
-      sym[2 * k + 1] = ws[k] >> 16;
-    }
+    for (int q = 0; q < HE_SPT / 8; ++q) pk[q] = v[q];
   } else {
 #pragma unroll
-    for (int k = 0; k < HE_SPT; ++k) sym[k] = (i0 + k < a.n) ? a.codes[i0 + k] : 0xffffffffu;
+    for (int q = 0; q < HE_SPT / 8; ++q) pk[q] = make_uint4(0, 0, 0, 0);
   }
-  unsigned long long ent[HE_SPT];
+  unsigned long long tail_e = 0;
+  const bool need_tail_sym = (wid == 0) && (base + HE_CH < a.n);
+  if (need_tail_sym) {
+    const int64_t i = base + HE_CH + lane;
+    if (i < a.n) tail_e = __ldg(a.tab + a.codes[i]);
+  }
+  auto sym_of = [&](int k) -> int {  // -1 past the end
+    if (full) return (int)sym_at(pk, k);
+    return (i0 + k < a.n) ? (int)a.codes[i0 + k] : -1;
+  };
+
+  // ---- lengths -> bits of this thread
   int tbits = 0;
 #pragma unroll
   for (int k = 0; k < HE_SPT; ++k) {
-    ent[k] = 0;
-    if (sym[k] != 0xffffffffu) {
-      ent[k] = __ldg(a.tab + sym[k]);
-      if ((ent[k] & 63) == 0) {  // not in the codebook (reported, contributes no bits)
-        const long long tag = ((i0 + k) << 16) | (long long)sym[k];
-        atomicMin(&a.info[(int)sym[k] >= a.nsym_span ? 1 : 3], tag);
-      }
+    const int s = sym_of(k);
+    if (s < 0) continue;
+    const int L = __ldg(a.len + s);
+    if (L == 0) {  // not in the codebook (reported, contributes no bits)
+      const long long tag = ((i0 + k) << 16) | (long long)s;
+      atomicMin(&a.info[s >= a.nsym_span ? 1 : 3], tag);
     }
-    tbits += (int)(ent[k] & 63);
+    tbits += L;
   }
 
   // ---- chunk scan of bit lengths
@@ -141,41 +162,47 @@ __global__ void __launch_bounds__(HE_THREADS) huff_encode_kernel(HEArgs a) {
   for (int w = tid; w < nwords; w += HE_THREADS) s_words[w] = 0;
   __syncthreads();
 
-  // ---- assemble this chunk's bits (aligned to the global word grid)
+  // ---- assemble this chunk's bits (aligned to the global word grid): a
+  // 64-bit accumulator per thread; words wholly inside the thread's bit range
+  // are plain shared stores, the (at most two) words shared with the
+  // neighbouring threads are atomicOr
   {
-    int p = sh + texcl;
-    int cur = p >> 5;
-    uint32_t acc = 0;
+    const int p0 = sh + texcl;
+    int w = p0 >> 5;
+    int nacc = p0 & 31;  // leading zero bits of the first word
+    unsigned long long acc = 0;
+    bool first = true;
+    auto push = [&](unsigned long long bits, int L) {  // nacc < 32, L <= 32
+      acc = (acc << L) | bits;
+      nacc += L;
+      if (nacc >= 32) {
+        const uint32_t word = (uint32_t)(acc >> (nacc - 32));
+        nacc -= 32;
+        if (first) atomicOr(&s_words[w], word);
+        else s_words[w] = word;
+        first = false;
+        ++w;
+      }
+    };
 #pragma unroll
     for (int k = 0; k < HE_SPT; ++k) {
-      int L = (int)(ent[k] & 63);
-      if (L == 0) continue;
-      unsigned long long X = (ent[k] >> 6) << (64 - L);  // left-aligned codeword
-      while (L > 0) {
-        const int o = p & 31, w = p >> 5;
-        const int take = L < 32 - o ? L : 32 - o;
-        const uint32_t bits = (uint32_t)(X >> (64 - take));
-        if (w != cur) {
-          if (acc) atomicOr(&s_words[cur], acc);
-          cur = w;
-          acc = 0;
-        }
-        acc |= bits << (32 - o - take);
-        X <<= take;
-        L -= take;
-        p += take;
+      const int s = sym_of(k);
+      if (s < 0) continue;
+      const unsigned long long e = __ldg(a.tab + s);
+      const int L = (int)(e & 63);
+      const unsigned long long cw = e >> 6;
+      if (L <= 32) {
+        push(cw, L);
+      } else {  // deep codeword: high part, then the low 32 bits
+        push(cw >> 32, L - 32);
+        push(cw & 0xffffffffull, 32);
       }
     }
-    if (acc) atomicOr(&s_words[cur], acc);
+    if (nacc > (first ? (p0 & 31) : 0)) atomicOr(&s_words[w], (uint32_t)(acc << (32 - nacc)));
   }
-  __syncthreads();
-
   // ---- complete the last (shared) word from the next chunk's leading symbols
-  if (wid == 0 && (e_local & 31) && base + HE_CH < a.n) {
-    const int64_t i = base + HE_CH + lane;
-    unsigned long long e = 0;
-    if (i < a.n) e = __ldg(a.tab + a.codes[i]);
-    const int L = (int)(e & 63);
+  if (need_tail_sym && (e_local & 31)) {
+    const int L = (int)(tail_e & 63);
     int x = L;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -186,7 +213,7 @@ __global__ void __launch_bounds__(HE_THREADS) huff_encode_kernel(HEArgs a) {
     const int need = 32 - (e_local & 31);
     if (L > 0 && excl < need) {
       const int take = L < need - excl ? L : need - excl;
-      const uint32_t bits = (uint32_t)(((e >> 6) << (64 - L)) >> (64 - take));
+      const uint32_t bits = (uint32_t)(((tail_e >> 6) << (64 - L)) >> (64 - take));
       const int o = (e_local + excl) & 31;
       atomicOr(&s_words[e_local >> 5], bits << (32 - o - take));
     }
@@ -207,7 +234,7 @@ __global__ void __launch_bounds__(HE_THREADS) huff_encode_kernel(HEArgs a) {
 
 extern "C" {
 
-size_t vlz_huff_table_bytes(void) { return 65536 * 8 + 65536 * 16; }
+size_t vlz_huff_table_bytes(void) { return vlz::HE_TAB + vlz::HE_LEN + 65536 * 16; }
 
 int vlz_huff_table(const uint16_t* h_syms, const uint8_t* h_lens, int32_t nsym, void* d_table,
                    void* stream) {
@@ -225,13 +252,14 @@ int vlz_huff_table(const uint16_t* h_syms, const uint8_t* h_lens, int32_t nsym, 
     if (i + 1 < nsym) code <<= (int)h_lens[i + 1] - L;
   }
   auto* tab = static_cast<unsigned long long*>(d_table);
-  unsigned long long* dst = tab + 65536;
-  if (cudaMemsetAsync(tab, 0, 65536 * 8, st) != cudaSuccess) return VLZ_E_CUDA;
+  auto* len = static_cast<uint8_t*>(d_table) + vlz::HE_TAB;
+  auto* dst = reinterpret_cast<unsigned long long*>(len + vlz::HE_LEN);
+  if (cudaMemsetAsync(tab, 0, vlz::HE_TAB + vlz::HE_LEN, st) != cudaSuccess) return VLZ_E_CUDA;
   // pageable source: returns once the bytes are staged, `staged` may go
   if (cudaMemcpyAsync(dst, staged.data(), staged.size() * 8, cudaMemcpyHostToDevice, st) !=
       cudaSuccess)
     return VLZ_E_CUDA;
-  vlz::he_table_kernel<<<(nsym + 255) / 256, 256, 0, st>>>(dst, nsym, tab);
+  vlz::he_table_kernel<<<(nsym + 255) / 256, 256, 0, st>>>(dst, nsym, tab, len);
   vlz::g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError() == cudaSuccess ? VLZ_OK : VLZ_E_CUDA;
 }
@@ -242,12 +270,13 @@ size_t vlz_huff_encode_ws_size(int64_t n) {
 }
 
 int vlz_huff_encode_device(const uint16_t* d_codes, int64_t n, const void* d_table,
-                           int32_t nsym_span, uint8_t* d_out, int64_t out_cap, int64_t* d_info,
+                           int32_t nsym_span, int32_t max_len, uint8_t* d_out, int64_t out_cap, int64_t* d_info,
                            void* d_ws, size_t ws_bytes, void* stream) {
   if (n < 0 || !d_table || !d_info || !d_ws || (n > 0 && (!d_codes || !d_out))) return VLZ_E_ARG;
   if ((reinterpret_cast<uintptr_t>(d_codes) & 15) || (reinterpret_cast<uintptr_t>(d_out) & 3))
     return VLZ_E_ARG;
-  if (ws_bytes < vlz_huff_encode_ws_size(n)) return VLZ_E_ARG;
+  if (ws_bytes < vlz_huff_encode_ws_size(n) || max_len < 1 || max_len > vlz::HE_MAXLEN)
+    return VLZ_E_ARG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t nchunks = n > 0 ? (n + vlz::HE_CH - 1) / vlz::HE_CH : 1;
   auto* ticket = static_cast<unsigned int*>(d_ws);
@@ -262,13 +291,23 @@ int vlz_huff_encode_device(const uint16_t* d_codes, int64_t n, const void* d_tab
   a.codes = d_codes;
   a.n = n;
   a.tab = static_cast<const unsigned long long*>(d_table);
+  a.len = static_cast<const uint8_t*>(d_table) + vlz::HE_TAB;
   a.nsym_span = nsym_span;
   a.out = reinterpret_cast<uint32_t*>(d_out);
   a.out_words = out_cap / 4;
   a.lb = lb;
   a.ticket = ticket;
   a.info = reinterpret_cast<long long*>(d_info);
-  vlz::huff_encode_kernel<<<(unsigned)nchunks, vlz::HE_THREADS, 0, st>>>(a);
+  // shared words: the chunk's bits at max_len per symbol, plus alignment
+  const size_t smem = ((size_t)vlz::HE_CH * max_len / 32 + 2) * 4;
+  static bool attr_set = false;  // opt in to > 48 KB once (up to 58-bit books)
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(vlz::huff_encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             ((size_t)vlz::HE_CH * vlz::HE_MAXLEN / 32 + 2) * 4) != cudaSuccess)
+      return VLZ_E_CUDA;
+    attr_set = true;
+  }
+  vlz::huff_encode_kernel<<<(unsigned)nchunks, vlz::HE_THREADS, smem, st>>>(a);
   vlz::g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError() == cudaSuccess ? VLZ_OK : VLZ_E_CUDA;
 }

@@ -288,7 +288,8 @@ def huffman_encode_device(codes: torch.Tensor, symbols: np.ndarray, lengths: np.
     out = torch.empty(cap, dtype=torch.uint8, device=dev)
     ws = torch.empty(int(lib.vlz_huff_encode_ws_size(n)), dtype=torch.uint8, device=dev)
     info = torch.empty(4, dtype=torch.int64, device=dev)
-    rc = lib.vlz_huff_encode_device(_ptr(c), n, _ptr(tab), int(syms.max()) + 1, _ptr(out), cap,
+    rc = lib.vlz_huff_encode_device(_ptr(c), n, _ptr(tab), int(syms.max()) + 1, maxlen,
+                                    _ptr(out), cap,
                                     _ptr(info), _ptr(ws), ws.numel(), st)
     if rc != 0:
         raise RuntimeError(f"vlz_huff_encode_device failed ({rc})")

@@ -62,6 +62,7 @@ def case(name, data, rel, b, pol, radius):
 
     def enc():
         lib.vlz_huff_encode_device(codes.data_ptr(), n, tab.data_ptr(), int(syms.max()) + 1,
+                                   int(lens.max()),
                                    out.data_ptr(), cap, info.data_ptr(), ws.data_ptr(),
                                    ws.numel(), None)
 
