@@ -31,6 +31,56 @@ namespace vlz {
 constexpr int FAST_STAGES = 2;
 constexpr int FAST_WARPS = 4;
 
+// per-lane vector moves of VPL (2, 4, 8) consecutive 32-bit values
+template <typename T>
+__device__ __forceinline__ T from_bits(int x) {
+  if constexpr (sizeof(T) == 4 && T(0.5f) != T(0)) return __int_as_float(x);  // float
+  else return (T)x;
+}
+template <int N, typename T>
+__device__ __forceinline__ void ld_vec(const T* p, T (&v)[N]) {
+  static_assert(sizeof(T) == 4, "32-bit lanes");
+  int t[N];
+  if constexpr (N == 8) {
+    const int4 a = *reinterpret_cast<const int4*>(p), b = *reinterpret_cast<const int4*>(p + 4);
+    t[0] = a.x; t[1] = a.y; t[2] = a.z; t[3] = a.w;
+    t[4 % N] = b.x; t[5 % N] = b.y; t[6 % N] = b.z; t[7 % N] = b.w;
+  } else if constexpr (N == 4) {
+    const int4 a = *reinterpret_cast<const int4*>(p);
+    t[0] = a.x; t[1] = a.y; t[2 % N] = a.z; t[3 % N] = a.w;
+  } else {
+    const int2 a = *reinterpret_cast<const int2*>(p);
+    t[0] = a.x; t[1] = a.y;
+  }
+#pragma unroll
+  for (int j = 0; j < N; ++j) v[j] = from_bits<T>(t[j]);
+}
+template <int N>
+__device__ __forceinline__ void st_vec(int* p, const int (&v)[N]) {
+  if constexpr (N == 8) {
+    *reinterpret_cast<int4*>(p) = make_int4(v[0], v[1], v[2], v[3]);
+    *reinterpret_cast<int4*>(p + 4) = make_int4(v[4], v[5], v[6], v[7]);
+  } else if constexpr (N == 4) {
+    *reinterpret_cast<int4*>(p) = make_int4(v[0], v[1], v[2], v[3]);
+  } else {
+    *reinterpret_cast<int2*>(p) = make_int2(v[0], v[1]);
+  }
+}
+// VPL u16 codes (low halves of c) with one 4/8/16-byte store
+template <int N>
+__device__ __forceinline__ void st_codes(uint16_t* p, const uint32_t (&c)[N]) {
+  if constexpr (N == 8) {
+    *reinterpret_cast<uint4*>(p) =
+        make_uint4(__byte_perm(c[0], c[1], 0x5410), __byte_perm(c[2], c[3], 0x5410),
+                   __byte_perm(c[4], c[5], 0x5410), __byte_perm(c[6], c[7], 0x5410));
+  } else if constexpr (N == 4) {
+    *reinterpret_cast<uint2*>(p) =
+        make_uint2(__byte_perm(c[0], c[1], 0x5410), __byte_perm(c[2], c[3], 0x5410));
+  } else {
+    *reinterpret_cast<uint32_t*>(p) = __byte_perm(c[0], c[1], 0x5410);
+  }
+}
+
 template <int ND, int B, int VPL>
 struct FastShape {
   using S = Shape<ND, B, VPL>;
@@ -44,7 +94,8 @@ struct FastShape {
   // ring of input planes + the previous plane's Dy Dx d (int32, 3-D only)
   static constexpr int PREV_BYTES = (ND == 3) ? PLANE_BYTES : 0;
   static constexpr int WARP_SMEM = (FAST_STAGES * STAGE_BYTES + PREV_BYTES + 64 + 127) / 128 * 128;
-  static constexpr int MINB = 4;  // CTAs per SM the register budget targets
+  // CTAs per SM the register budget targets (VPL 8: 24 KB of smem per warp)
+  static constexpr int MINB = VPL == 8 ? 2 : 4;
 };
 
 template <int ND, int B, int VPL>
@@ -187,8 +238,10 @@ __device__ __forceinline__ void fast_tile(const FastArgs& fa, uint32_t tile, con
   if (ND == 3) {  // previous-plane state starts at zero (Dz zero fill)
 #pragma unroll 1
     for (int yl = 0; yl < BY; ++yl) {
-      if (VPL == 4) *reinterpret_cast<int4*>(pplane + yl * W) = make_int4(0, 0, 0, 0);
-      else *reinterpret_cast<int2*>(pplane + yl * W) = make_int2(0, 0);
+      int z[VPL];
+#pragma unroll
+      for (int j = 0; j < VPL; ++j) z[j] = 0;
+      st_vec<VPL>(pplane + yl * W, z);
     }
   }
   int run = 0;
@@ -200,6 +253,11 @@ __device__ __forceinline__ void fast_tile(const FastArgs& fa, uint32_t tile, con
   KAcc<K> face[ND];
   long long tcnt = 0;
   uint16_t* cptr = a.codes + bstart + xin;  // advances by ex per row
+  // interior tiles stage their codes in shared memory (see the copy-out)
+  constexpr bool STAGE_CODES = INTERIOR && F::SPLIT == 1 && BX == 8;  // 16-byte block rows
+  const int64_t bstart0 =
+      block_start(g, tc.bz, tc.by, (int64_t)tc.wx * (W / BX), BZ, BY, BX, ez, ey);
+  const int64_t bsize = (int64_t)ez * BY * BX;  // codes per block of this layer
 
   for (int zl = 0; zl < ez; ++zl) {
     int prow[VPL];
@@ -208,29 +266,30 @@ __device__ __forceinline__ void fast_tile(const FastArgs& fa, uint32_t tile, con
     int psum = 0;  // |sum of a plane| < BY * W / 32 * VPL * 2^24 < 2^31
     for (int part = 0; part < F::SPLIT; ++part) {
     const float* plane = ring + cons.stage * F::STAGE_FLOATS + lane * VPL;
+    unsigned char* const stage_bytes = reinterpret_cast<unsigned char*>(ring + cons.stage * F::STAGE_FLOATS);
     mbar_wait(&bars[cons.stage], cons.parity);
 #pragma unroll 2
     for (int r = 0; r < F::STAGE_ROWS; ++r) {
       const int yl = part * F::STAGE_ROWS + r;
       if (!INTERIOR && yl >= ey) break;
       float v[VPL];
-      if (VPL == 4) {
-        const float4 f = *reinterpret_cast<const float4*>(plane + r * W);
-        v[0] = f.x; v[1 % VPL] = f.y; v[2 % VPL] = f.z; v[3 % VPL] = f.w;
-      } else {
-        const float2 f = *reinterpret_cast<const float2*>(plane + r * W);
-        v[0] = f.x; v[1 % VPL] = f.y;
-      }
+      ld_vec<VPL>(plane + r * W, v);
       // ---- float32 fast prequantization; nb = biased bit pattern of n
       unsigned nb[VPL];
       bool allok = true;
+      // paired FP32 (FMUL2/FADD2/FFMA2, sm_100): the same IEEE RN operations
+      // element by element, two per instruction
 #pragma unroll
-      for (int j = 0; j < VPL; ++j) {
-        const float qq = __fmul_rn(v[j], q.inv32);
-        const float r = __fadd_rn(qq, 12582912.0f);
-        nb[j] = __float_as_uint(r);
-        const float e = __fsub_rn(qq, __fsub_rn(r, 12582912.0f));
-        allok = allok && (fabsf(e) < __fmaf_rn(fabsf(qq), -q.kq, q.lim0));
+      for (int j = 0; j < VPL; j += 2) {
+        const float2 qq = __fmul2_rn(make_float2(v[j], v[j + 1]), make_float2(q.inv32, q.inv32));
+        const float2 r = __fadd2_rn(qq, make_float2(12582912.0f, 12582912.0f));
+        nb[j] = __float_as_uint(r.x);
+        nb[j + 1] = __float_as_uint(r.y);
+        const float2 rn = __fadd2_rn(r, make_float2(-12582912.0f, -12582912.0f));  // exact
+        const float2 e = __ffma2_rn(rn, make_float2(-1.0f, -1.0f), qq);              // qq - n, exact
+        const float2 lim = __ffma2_rn(make_float2(fabsf(qq.x), fabsf(qq.y)),
+                                      make_float2(-q.kq, -q.kq), make_float2(q.lim0, q.lim0));
+        allok = allok && (fabsf(e.x) < lim.x) && (fabsf(e.y) < lim.y);
       }
       if (!INTERIOR) {
 #pragma unroll
@@ -287,15 +346,8 @@ __device__ __forceinline__ void fast_tile(const FastArgs& fa, uint32_t tile, con
       if (ND == 3) {
         int* pp = pplane + yl * W;
         int prev[VPL];
-        if (VPL == 4) {
-          const int4 p4 = *reinterpret_cast<const int4*>(pp);
-          prev[0] = p4.x; prev[1 % VPL] = p4.y; prev[2 % VPL] = p4.z; prev[3 % VPL] = p4.w;
-          *reinterpret_cast<int4*>(pp) = make_int4(dl[0], dl[1 % VPL], dl[2 % VPL], dl[3 % VPL]);
-        } else {
-          const int2 p2 = *reinterpret_cast<const int2*>(pp);
-          prev[0] = p2.x; prev[1 % VPL] = p2.y;
-          *reinterpret_cast<int2*>(pp) = make_int2(dl[0], dl[1 % VPL]);
-        }
+        ld_vec<VPL>(pp, prev);
+        st_vec<VPL>(pp, dl);
 #pragma unroll
         for (int j = 0; j < VPL; ++j) dl[j] -= prev[j];
       }
@@ -325,13 +377,16 @@ __device__ __forceinline__ void fast_tile(const FastArgs& fa, uint32_t tile, con
         bad_origin = badm & 1u;
         v_origin = v[0];
       }
-      if (vec_store) {
-        if (VPL == 4) {
-          *reinterpret_cast<uint2*>(cptr) =
-              make_uint2(__byte_perm(c[0], c[1 % VPL], 0x5410), __byte_perm(c[2 % VPL], c[3 % VPL], 0x5410));
-        } else {
-          *reinterpret_cast<uint32_t*>(cptr) = __byte_perm(c[0], c[1 % VPL], 0x5410);
-        }
+      if (STAGE_CODES) {
+        // this row's codes go into the consumed input row (16-byte chunks
+        // rotated by row: conflict-free here and in the copy-out below)
+        constexpr int CPR = W / 8;
+        const int cbyte = lane * VPL * 2;
+        const int pos = ((cbyte >> 4) + r * (BX / 8)) % CPR;
+        st_codes<VPL>(reinterpret_cast<uint16_t*>(stage_bytes + r * W * 4 + pos * 16 +
+                                                  (cbyte & 15)), c);
+      } else if (vec_store) {
+        st_codes<VPL>(cptr, c);
       } else if (lane_valid) {
 #pragma unroll
         for (int j = 0; j < VPL; ++j)
@@ -385,6 +440,23 @@ __device__ __forceinline__ void fast_tile(const FastArgs& fa, uint32_t tile, con
             if (x0) face[ND - 1].add(d);
           }
         }
+      }
+    }
+    if (STAGE_CODES) {
+      // copy the plane's codes out: each block's plane is BY*BX contiguous
+      // codes, so every 8 lanes store 128 contiguous bytes (full L2 lines
+      // instead of one 8-byte piece per block row)
+      __syncwarp();
+      constexpr int CPR = W / 8, KB = BY * BX / 8, NCH = BY * CPR;
+      uint16_t* const cbase = a.codes + bstart0 + (int64_t)zl * (BY * BX);
+#pragma unroll
+      for (int i = 0; i < NCH / 32; ++i) {
+        const int t = i * 32 + lane;
+        const int j = t / KB, k = t % KB;
+        const int r = k / (BX / 8), cx = k % (BX / 8);
+        const int pos = (j * (BX / 8) + cx + r * (BX / 8)) % CPR;
+        const uint4 val = *reinterpret_cast<const uint4*>(stage_bytes + r * W * 4 + pos * 16);
+        *reinterpret_cast<uint4*>(cbase + j * bsize + k * 8) = val;
       }
     }
     // release the stage and refill it FAST_STAGES half planes ahead

@@ -11,6 +11,9 @@
 #ifndef VLZ_VPL_3D8
 #define VLZ_VPL_3D8 4  // columns per lane for 3-D b=8 tiles (window 32*VPL)
 #endif
+#ifndef VLZ_VPL_C3D8
+#define VLZ_VPL_C3D8 4  // ... for the 3-D b=8 compress tiles (one block row per lane)
+#endif
 
 namespace vlz {
 
@@ -56,7 +59,8 @@ cudaError_t launch_compress_nd3(int B, int mode, const CompressArgs& a, cudaStre
 cudaError_t launch_decompress(int nd, int B, bool u32, const DecompressArgs& a, cudaStream_t st);
 
 // window width (columns per warp tile) used for (nd, B)
-inline int vpl_for(int nd, int B) {
+inline int vpl_for(int nd, int B, bool compress = false) {
+  if (compress && nd == 3 && B == 8) return VLZ_VPL_C3D8;
   if (nd == 1 && B == 256) return 8;
   if (nd == 3 && B == 64) return 2;
   if (nd >= 2 && B == 16) return 2;

@@ -83,7 +83,8 @@ bool valid_geom(const vlz_geom* g) {
   return true;
 }
 
-bool make_geo(const vlz_geom* gg, Geo& g) {
+// compress = true: the tile window of the compress kernels (vpl_for)
+bool make_geo(const vlz_geom* gg, Geo& g, bool compress = false) {
   if (!valid_geom(gg)) return false;
   const int b = gg->block_edge;
   int64_t D[3] = {1, 1, 1};
@@ -95,7 +96,7 @@ bool make_geo(const vlz_geom* gg, Geo& g) {
   g.P0 = (D[0] + BZ - 1) / BZ;
   g.P1 = (D[1] + BY - 1) / BY;
   g.P2 = (D[2] + BX - 1) / BX;
-  const int W = 32 * vpl_for(gg->nd, b);
+  const int W = 32 * vpl_for(gg->nd, b, compress);
   g.NW = (D[2] + W - 1) / W;
   g.ntiles = g.P0 * g.P1 * g.NW;
   g.nblocks = g.P0 * g.P1 * g.P2;
@@ -330,7 +331,7 @@ __attribute__((visibility("hidden"))) int vlz_internal_compress_begin(const floa
                                vlz_result* d_result, long long* stats, void* d_ws,
                                size_t ws_bytes, cudaStream_t st) {
   Geo g;
-  if (!make_geo(gg, g) || !valid_params(p) || !(p->eb > 0.0) || !d_in || !d_codes ||
+  if (!make_geo(gg, g, true) || !valid_params(p) || !(p->eb > 0.0) || !d_in || !d_codes ||
       !d_counts || !d_result || !d_ws)
     return VLZ_E_ARG;
   WS w = carve(g, d_ws);
@@ -370,7 +371,7 @@ __attribute__((visibility("hidden"))) int vlz_internal_compress_finish(const flo
                                 void* d_ws, size_t ws_bytes, cudaStream_t st,
                                 unsigned long long* patch_list, unsigned int* patch_count) {
   Geo g;
-  if (!make_geo(gg, g) || !valid_params(p) || !d_outliers || !d_result || !d_ws)
+  if (!make_geo(gg, g, true) || !valid_params(p) || !d_outliers || !d_result || !d_ws)
     return VLZ_E_ARG;
   WS w = carve(g, d_ws);
   if (ws_bytes < w.bytes) return VLZ_E_ARG;
@@ -409,7 +410,7 @@ int vlz_dq_compress(const float* d_in, const vlz_geom* g, const vlz_params* p, u
                     vlz_result* d_result, void* d_ws, size_t ws_bytes, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   Geo gg;
-  if (!make_geo(g, gg)) return VLZ_E_ARG;
+  if (!make_geo(g, gg, true)) return VLZ_E_ARG;
   WS w = carve(gg, d_ws);
   int rc = vlz_internal_compress_begin(d_in, g, p, d_codes, d_counts, d_scalars, d_result, w.stats,
                                d_ws, ws_bytes, st);
