@@ -66,18 +66,19 @@ __device__ __forceinline__ void st_vec(int* p, const int (&v)[N]) {
     *reinterpret_cast<int2*>(p) = make_int2(v[0], v[1]);
   }
 }
-// VPL u16 codes (low halves of c) with one 4/8/16-byte store
+// VPL u16 codes (low halves of c, plus `add` per packed pair) with one
+// 4/8/16-byte store
 template <int N>
-__device__ __forceinline__ void st_codes(uint16_t* p, const uint32_t (&c)[N]) {
+__device__ __forceinline__ void st_codes(uint16_t* p, const uint32_t (&c)[N], uint32_t add = 0u) {
   if constexpr (N == 8) {
     *reinterpret_cast<uint4*>(p) =
-        make_uint4(__byte_perm(c[0], c[1], 0x5410), __byte_perm(c[2], c[3], 0x5410),
-                   __byte_perm(c[4], c[5], 0x5410), __byte_perm(c[6], c[7], 0x5410));
+        make_uint4(__byte_perm(c[0], c[1], 0x5410) + add, __byte_perm(c[2], c[3], 0x5410) + add,
+                   __byte_perm(c[4], c[5], 0x5410) + add, __byte_perm(c[6], c[7], 0x5410) + add);
   } else if constexpr (N == 4) {
     *reinterpret_cast<uint2*>(p) =
-        make_uint2(__byte_perm(c[0], c[1], 0x5410), __byte_perm(c[2], c[3], 0x5410));
+        make_uint2(__byte_perm(c[0], c[1], 0x5410) + add, __byte_perm(c[2], c[3], 0x5410) + add);
   } else {
-    *reinterpret_cast<uint32_t*>(p) = __byte_perm(c[0], c[1], 0x5410);
+    *reinterpret_cast<uint32_t*>(p) = __byte_perm(c[0], c[1], 0x5410) + add;
   }
 }
 
@@ -255,6 +256,7 @@ __device__ __forceinline__ void fast_tile(const FastArgs& fa, uint32_t tile, con
   uint16_t* cptr = a.codes + bstart + xin;  // advances by ex per row
   // interior tiles stage their codes in shared memory (see the copy-out)
   constexpr bool STAGE_CODES = INTERIOR && F::SPLIT == 1 && BX == 8;  // 16-byte block rows
+  const int stage_chunk0 = (lane * VPL * 2) >> 4, stage_sub = (lane * VPL * 2) & 15;
   const int64_t bstart0 =
       block_start(g, tc.bz, tc.by, (int64_t)tc.wx * (W / BX), BZ, BY, BX, ez, ey);
   const int64_t bsize = (int64_t)ez * BY * BX;  // codes per block of this layer
@@ -351,25 +353,16 @@ __device__ __forceinline__ void fast_tile(const FastArgs& fa, uint32_t tile, con
 #pragma unroll
         for (int j = 0; j < VPL; ++j) dl[j] -= prev[j];
       }
-      // ---- postquantization: code = delta + R, or 0 for an outlier
-      bool out[VPL];
-      uint32_t c[VPL];
-      bool anyout = false;
+      // ---- postquantization: code = delta + R, or 0 for an outlier.
+      // u = delta + R - 1 is in range iff u <= 2R - 2 (unsigned): one max per
+      // lane tells whether the warp needs the per-element outlier path; in
+      // the common path the +1 is added to the packed code pairs
+      unsigned u[VPL];
+      unsigned umax = 0;
 #pragma unroll
       for (int j = 0; j < VPL; ++j) {
-        const int u = dl[j] + (R - 1);
-        out[j] = (unsigned)u > span;
-        c[j] = out[j] ? 0u : (uint32_t)(u + 1);
-        anyout = anyout || out[j];
-      }
-      if (badm) {  // rare, lane-local: narrowed reconstruction misses the bound
-#pragma unroll
-        for (int j = 0; j < VPL; ++j)
-          if ((badm >> j) & 1u) {
-            out[j] = true;
-            c[j] = 0u;
-          }
-        anyout = true;
+        u[j] = (unsigned)(dl[j] + (R - 1));
+        umax = u[j] > umax ? u[j] : umax;
       }
       const bool origin_row = (zl == 0) && (yl == 0) && xhead;
       if (origin_row) {
@@ -377,27 +370,18 @@ __device__ __forceinline__ void fast_tile(const FastArgs& fa, uint32_t tile, con
         bad_origin = badm & 1u;
         v_origin = v[0];
       }
-      if (STAGE_CODES) {
-        // this row's codes go into the consumed input row (16-byte chunks
-        // rotated by row: conflict-free here and in the copy-out below)
-        constexpr int CPR = W / 8;
-        const int cbyte = lane * VPL * 2;
-        const int pos = ((cbyte >> 4) + r * (BX / 8)) % CPR;
-        st_codes<VPL>(reinterpret_cast<uint16_t*>(stage_bytes + r * W * 4 + pos * 16 +
-                                                  (cbyte & 15)), c);
-      } else if (vec_store) {
-        st_codes<VPL>(cptr, c);
-      } else if (lane_valid) {
-#pragma unroll
-        for (int j = 0; j < VPL; ++j)
-          if (j < nvalid) cptr[j] = (uint16_t)c[j];
-      }
-      cptr += ex;
-      // ---- outliers (rare): rank inside the block in traversal order
-      if (__any_sync(FULL, anyout)) {
+      unsigned cadd = 0x00010001u;  // per 16-bit half: code = u + 1
+      if (__any_sync(FULL, umax > span || badm != 0u)) {
+        // rare: outliers (code 0; narrowing failures included), ranked inside
+        // the block in traversal order
         unsigned om = 0;
 #pragma unroll
-        for (int j = 0; j < VPL; ++j) om |= out[j] ? (1u << j) : 0u;
+        for (int j = 0; j < VPL; ++j) {
+          const bool o = u[j] > span || ((badm >> j) & 1u);
+          u[j] = o ? 0u : u[j] + 1u;
+          om |= o ? (1u << j) : 0u;
+        }
+        cadd = 0u;
         om &= vmask;
         if (origin_row) om &= ~1u;
         int tot;
@@ -409,6 +393,21 @@ __device__ __forceinline__ void fast_tile(const FastArgs& fa, uint32_t tile, con
           if ((om >> j) & 1u) slot[k++] = v[j];
         run += tot;
       }
+      if (STAGE_CODES) {
+        // this row's codes go into the consumed input row (16-byte chunks
+        // rotated by row: conflict-free here and in the copy-out below)
+        constexpr int CPR = W / 8;
+        const int pos = (stage_chunk0 + r * (BX / 8)) & (CPR - 1);
+        st_codes<VPL>(reinterpret_cast<uint16_t*>(stage_bytes + r * W * 4 + pos * 16 +
+                                                  stage_sub), u, cadd);
+      } else if (vec_store) {
+        st_codes<VPL>(cptr, u, cadd);
+      } else if (lane_valid) {
+#pragma unroll
+        for (int j = 0; j < VPL; ++j)
+          if (j < nvalid) cptr[j] = (uint16_t)(u[j] + (cadd & 1u));
+      }
+      cptr += ex;
       // ---- padding statistics on d = nb - bias (in-bounds columns only)
       if (MODE == MODE_GLOBAL) {
         if (K == 3) {
