@@ -281,7 +281,7 @@ def run_ours(args):
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.5)
-    for _ in range(args.warmup):
+    for _ in range(max(args.warmup, 1)):  # >= 1 step so the statuses below exist
         n_out = step(False)
     torch.cuda.synchronize()
     r = _lib.Result()
