@@ -21,7 +21,11 @@
 //    codes are fetched synchronously (partial blocks are not 4-byte aligned)
 //    and positions beyond the array read as "delta 0" -- they trail every
 //    valid position of their block in x and y, so they never feed one;
-//  * output rows leave with 16-byte stores straight from registers.
+//  * output rows leave with 16-byte stores straight from registers; rows are
+//    unrolled by two so that the dequantisation of one row overlaps the
+//    scans of the next;
+//  * grids of full 8x8x8 blocks take the TMA variant (dq_decompress_tma_kernel):
+//    one tensor load per plane brings 16 block planes, 128-byte swizzled.
 #pragma once
 
 #include "dq_compress_fast.cuh"
@@ -48,6 +52,7 @@ __host__ __device__ constexpr int dfast_smem_bytes() {
 }
 
 struct DFastArgs {
+  CUtensorMap tmap;  // TMA path: codes as (64, BZ, nblocks) uint16, box (64, 1, NBLK)
   DecompressArgs d;
   unsigned int* redo_count;
   long long* redo_list;
@@ -66,6 +71,7 @@ template <int ND, int B, int VPL>
 struct DProducer {
   using S = Shape<ND, B, VPL>;
   using F = DFastShape<ND, B, VPL>;
+  static constexpr bool TMAP = false;
   uint32_t tile;
   int zl, ez;
   const uint16_t* src;  // this lane's codes in plane 0, row 0 of the current tile
@@ -113,12 +119,60 @@ struct DProducer {
   }
 };
 
-template <int ND, int B, int VPL, bool EDGE>
+// TMA producer (3-D b=8 grids whose blocks are all full, so block b's codes
+// start at b * 512): one tensor load per plane brings plane zl of the
+// window's NBLK consecutive blocks, [block][64 codes], 128-byte swizzled so
+// that the consumer's row reads (all lanes on the same row of different
+// blocks) are conflict-free.  mbarrier ring as in the compress kernel.
+template <int ND, int B, int VPL>
+struct DTProducer {
+  using S = Shape<ND, B, VPL>;
+  using F = DFastShape<ND, B, VPL>;
+  static constexpr bool TMAP = true;
+  uint32_t tile;
+  int zl, ez;
+  int b0;  // first block of the window
+  int stage;
+  __device__ __forceinline__ void seek(const Geo& g, uint32_t nwarps) {
+    while (tile < (uint32_t)g.ntiles) {
+      const TileXY c = decode_tile(g, tile);
+      if (tile_interior<ND, B, VPL>(g, c)) {
+        ez = (int)imin64(S::BZ, g.D0 - (int64_t)c.bz * S::BZ);
+        b0 = (int)(((int64_t)c.bz * g.P1 + c.by) * g.P2 + (int64_t)c.wx * F::NBLK);
+        zl = 0;
+        return;
+      }
+      tile += nwarps;
+    }
+  }
+  __device__ __forceinline__ void start(const Geo& g, uint32_t t, uint32_t nwarps) {
+    tile = t;
+    stage = 0;
+    seek(g, nwarps);
+  }
+  __device__ __forceinline__ void issue(const Geo& g, const CUtensorMap* tmap,
+                                        unsigned char* ring, uint64_t* bars, int lane,
+                                        uint32_t nwarps) {
+    if (tile >= (uint32_t)g.ntiles) return;
+    if (lane == 0) {
+      uint64_t* bar = &bars[stage];
+      mbar_arrive_expect_tx(bar, (uint32_t)F::STAGE_BYTES);
+      tma_load_3d(ring + stage * F::STAGE_BYTES, tmap, 0, zl, b0, bar);
+    }
+    if (++stage == FAST_STAGES) stage = 0;
+    if (++zl >= ez) {
+      tile += nwarps;
+      seek(g, nwarps);
+    }
+  }
+};
+
+template <int ND, int B, int VPL, bool EDGE, class Prod>
 __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, const TileXY& tc,
-                                           int lane, unsigned char* ring,
-                                           DProducer<ND, B, VPL>& prod,
-                                           Consumer<ND, B, VPL>& cons, uint32_t nwarps,
-                                           long long& sent_acc) {
+                                           int lane, unsigned char* ring, uint64_t* bars,
+                                           Prod& prod, Consumer<ND, B, VPL>& cons,
+                                           uint32_t nwarps, long long& sent_acc) {
+  constexpr bool TMAP = Prod::TMAP;
   using S = Shape<ND, B, VPL>;
   using F = DFastShape<ND, B, VPL>;
   constexpr int BZ = S::BZ, BY = S::BY, BX = S::BX, W = S::W, LPB = S::LPB;
@@ -169,7 +223,7 @@ __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, c
   }
   int run = 0;
   bool badcode = false;
-  unsigned dmag = 0;  // OR of (d + 2^27): stays < 2^28 iff every |d| < 2^27
+  int dmax = 0, dmin = 0;  // range of every d of the tile (exact iff within +-2^27)
   float* orow = a.out + (z0 * g.D1 + y0) * g.D2 + xl0;
   const unsigned char* const slot0 = ring + lane * F::LANE_BYTES;
 
@@ -194,6 +248,9 @@ __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, c
           *reinterpret_cast<unsigned*>(fill + yl * 32 * F::LANE_BYTES) = v[0] | (v[1 % VPL] << 16);
       }
       slot = slot0;
+    } else if (TMAP) {
+      slot = ring + cons.stage * F::STAGE_BYTES;  // swizzled [block][64 codes]
+      mbar_wait(&bars[cons.stage], cons.parity);
     } else {
       slot = slot0 + cons.stage * F::STAGE_BYTES;
       cp_async_wait<FAST_STAGES - 1>();
@@ -203,18 +260,21 @@ __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, c
     for (int j = 0; j < VPL; ++j) grow[j] = (ND == 3) ? 0 : s0;
     int* pp = pplane;
     float* dst = orow;
-#pragma unroll 1
+#pragma unroll 2
     for (int yl = 0; yl < ey; ++yl) {
       unsigned c[VPL];
+      const unsigned char* rowp = slot;
+      if (TMAP)  // block blk, row yl: 16-byte chunk yl of line blk, XOR-swizzled
+        rowp = slot + blk * 128 + (((yl ^ blk) & 7) << 4) + (xin * 2);
       if (VPL == 4) {
-        const uint2 pk = *reinterpret_cast<const uint2*>(slot);
+        const uint2 pk = *reinterpret_cast<const uint2*>(rowp);
         c[0] = pk.x & 0xffffu; c[1 % VPL] = pk.x >> 16;
         c[2 % VPL] = pk.y & 0xffffu; c[3 % VPL] = pk.y >> 16;
       } else {
-        const unsigned pk = *reinterpret_cast<const unsigned*>(slot);
+        const unsigned pk = *reinterpret_cast<const unsigned*>(rowp);
         c[0] = pk & 0xffffu; c[1 % VPL] = pk >> 16;
       }
-      slot += 32 * F::LANE_BYTES;
+      if (!TMAP) slot += 32 * F::LANE_BYTES;
       int ep[VPL];
       if (ND == 3) {
         if (VPL == 4) {
@@ -304,8 +364,16 @@ __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, c
         const int gv = h[j] + grow[j];
         grow[j] = gv;
         dv[j] = gv + ep[j];  // = d (primed state)
-        dmag |= (unsigned)(dv[j] + (1 << 27));
-        o[j] = __double2float_rn(__dmul_rn((double)dv[j], a.q.twoeb));
+        // float64(d) without the quarter-rate I2F: 2^52 + 2^31 + d has d in
+        // its low word exactly, one DADD removes the offset (exact)
+        const double dd = __dadd_rn(__hiloint2double(0x43300000, dv[j] ^ (int)0x80000000),
+                                    -4503601774854144.0);
+        o[j] = __double2float_rn(__dmul_rn(dd, a.q.twoeb));
+      }
+#pragma unroll
+      for (int j = 0; j < VPL; j += 2) {
+        dmax = max(dmax, max(dv[j], dv[j + 1 < VPL ? j + 1 : j]));
+        dmin = min(dmin, min(dv[j], dv[j + 1 < VPL ? j + 1 : j]));
       }
       if (smask) {
 #pragma unroll
@@ -325,12 +393,17 @@ __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, c
       dst += g.D2;
     }
     orow += g.D1 * g.D2;
-    if (!EDGE) {
+    if constexpr (TMAP) {
+      __syncwarp();
+      fence_proxy_async_smem();
+      prod.issue(g, &fa.tmap, ring, bars, lane, nwarps);
+      cons.advance();
+    } else if (!EDGE) {
       prod.issue(g, codes, ring, nwarps, lane);
       cons.advance();
     }
   }
-  wide |= dmag >= (1u << 28);
+  wide |= dmax >= (1 << 27) || dmin < -(1 << 27);
   if (__any_sync(FULL, wide)) {
     if (lane == 0) fa.redo_list[atomicAdd(fa.redo_count, 1u)] = tile;
     return;
@@ -347,7 +420,8 @@ __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, c
 }
 
 template <int ND, int B, int VPL>
-__global__ void __launch_bounds__(FAST_WARPS * 32, 4) dq_decompress_fast_kernel(DFastArgs fa) {
+__global__ void __launch_bounds__(FAST_WARPS * 32, 4)
+    dq_decompress_fast_kernel(const __grid_constant__ DFastArgs fa) {
   using F = DFastShape<ND, B, VPL>;
   extern __shared__ __align__(128) unsigned char smem_dfast[];
   const int lane = threadIdx.x & 31;
@@ -366,7 +440,56 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, 4) dq_decompress_fast_kernel(
   for (uint32_t tile = first; tile < (uint32_t)g.ntiles; tile += nwarps) {
     const TileXY tc = decode_tile(g, tile);
     if (!tile_interior<ND, B, VPL>(g, tc)) continue;  // dq_decompress_edge_kernel
-    dfast_tile<ND, B, VPL, false>(fa, tile, tc, lane, ring, prod, cons, nwarps, sent);
+    dfast_tile<ND, B, VPL, false>(fa, tile, tc, lane, ring, nullptr, prod, cons, nwarps, sent);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sent += __shfl_xor_sync(FULL, sent, o);
+  if (lane == 0 && sent) atomicAdd(fa.d.sentinels, (unsigned long long)sent);
+}
+
+// TMA variant (DTProducer): per-warp [stages | previous plane | barriers],
+// 1024-byte aligned for the 128-byte swizzle
+template <int ND, int B, int VPL>
+struct DTmaShape {
+  using F = DFastShape<ND, B, VPL>;
+  static constexpr int BAR_OFF = FAST_STAGES * F::STAGE_BYTES + F::PREV_BYTES;
+  static constexpr int WARP_SMEM = (BAR_OFF + 64 + 1023) / 1024 * 1024;
+};
+template <int ND, int B, int VPL>
+__host__ __device__ constexpr int dtma_smem_bytes() {
+  return FAST_WARPS * DTmaShape<ND, B, VPL>::WARP_SMEM + 1024;
+}
+
+template <int ND, int B, int VPL>
+__global__ void __launch_bounds__(FAST_WARPS * 32, 4)
+    dq_decompress_tma_kernel(const __grid_constant__ DFastArgs fa) {
+  using T = DTmaShape<ND, B, VPL>;
+  extern __shared__ __align__(1024) unsigned char smem_dtma[];
+  unsigned char* base = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_dtma) + 1023) & ~uintptr_t(1023));
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  unsigned char* ring = base + (size_t)wib * T::WARP_SMEM;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + T::BAR_OFF);
+  const Geo& g = fa.d.g;
+  if (lane == 0) {
+    for (int s = 0; s < FAST_STAGES; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  if (lane == 0) prefetch_tmap(&fa.tmap);
+
+  const uint32_t nwarps = gridDim.x * FAST_WARPS;
+  const uint32_t first = blockIdx.x * FAST_WARPS + wib;
+  DTProducer<ND, B, VPL> prod;
+  prod.start(g, first, nwarps);
+  for (int s = 0; s < FAST_STAGES; ++s) prod.issue(g, &fa.tmap, ring, bars, lane, nwarps);
+  Consumer<ND, B, VPL> cons{0, 0u};
+  long long sent = 0;
+  for (uint32_t tile = first; tile < (uint32_t)g.ntiles; tile += nwarps) {
+    const TileXY tc = decode_tile(g, tile);
+    if (!tile_interior<ND, B, VPL>(g, tc)) continue;  // dq_decompress_edge_kernel
+    dfast_tile<ND, B, VPL, false>(fa, tile, tc, lane, ring, bars, prod, cons, nwarps, sent);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) sent += __shfl_xor_sync(FULL, sent, o);
@@ -383,7 +506,8 @@ __host__ __device__ inline int64_t edge_tile_count(const Geo& g) {
 }
 
 template <int ND, int B, int VPL>
-__global__ void __launch_bounds__(FAST_WARPS * 32, 4) dq_decompress_edge_kernel(DFastArgs fa) {
+__global__ void __launch_bounds__(FAST_WARPS * 32, 4)
+    dq_decompress_edge_kernel(const __grid_constant__ DFastArgs fa) {
   using S = Shape<ND, B, VPL>;
   using F = DFastShape<ND, B, VPL>;
   extern __shared__ __align__(128) unsigned char smem_dfast[];
@@ -412,7 +536,8 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, 4) dq_decompress_edge_kernel(
       tc.wx = (uint32_t)(j % nxb);
     }
     const uint32_t tile = (uint32_t)(((int64_t)tc.bz * g.P1 + tc.by) * g.NW + tc.wx);
-    dfast_tile<ND, B, VPL, true>(fa, tile, tc, lane, ring, prod, cons, (uint32_t)nwarps, sent);
+    dfast_tile<ND, B, VPL, true>(fa, tile, tc, lane, ring, nullptr, prod, cons, (uint32_t)nwarps,
+                                 sent);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) sent += __shfl_xor_sync(FULL, sent, o);

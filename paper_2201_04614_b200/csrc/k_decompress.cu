@@ -6,8 +6,23 @@
 //   everything else: dq_decompress_kernel (int64)
 #include "dq_decompress_fast.cuh"
 #include "launch.cuh"
+#include "launch_compress.cuh"  // encode_tiled
 
 namespace vlz {
+
+// codes of a grid of full 8x8x8 blocks as a (64, 8, nblocks) uint16 tensor:
+// box (64, 1, 16) = plane zl of 16 consecutive blocks, 128-byte swizzle
+static bool make_code_map(CUtensorMap* m, const void* codes, int64_t nblocks) {
+  EncodeTiledFn fn = encode_tiled();
+  if (!fn) return false;
+  const cuuint64_t dims[3] = {64, 8, (cuuint64_t)nblocks};
+  const cuuint64_t strides[2] = {128, 1024};
+  const cuuint32_t box[3] = {64, 1, 16};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, const_cast<void*>(codes), dims, strides, box,
+            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 
 template <int ND, int B>
 constexpr bool has_dfast() {
@@ -24,8 +39,20 @@ static cudaError_t run_d(bool u32, const DecompressArgs& a, cudaStream_t st) {
                          a.redo_list != nullptr && a.g.ntiles < (1ll << 30) &&
                          (a.q.twoeb < 1e300);
     if (aligned) {
+      DFastArgs fa{};
+      fa.d = a;
+      fa.redo_count = const_cast<unsigned int*>(a.redo_count);
+      fa.redo_list = const_cast<long long*>(a.redo_list);
       auto kern = dq_decompress_fast_kernel<ND, B, VPL>;
-      constexpr int fsmem = dfast_smem_bytes<ND, B, VPL>();
+      int fsmem = dfast_smem_bytes<ND, B, VPL>();
+      if constexpr (ND == 3 && B == 8 && VPL == 4) {
+        // every block full (block b starts at b * 512): TMA tensor loads
+        if (a.g.D0 % 8 == 0 && a.g.D1 % 8 == 0 && a.g.D2 % 8 == 0 &&
+            a.g.nblocks < (1ll << 31) && make_code_map(&fa.tmap, a.codes, a.g.nblocks)) {
+          kern = dq_decompress_tma_kernel<ND, B, VPL>;
+          fsmem = dtma_smem_bytes<ND, B, VPL>();
+        }
+      }
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem);
       if (e != cudaSuccess) return e;
       int per_sm = 0;
@@ -36,7 +63,6 @@ static cudaError_t run_d(bool u32, const DecompressArgs& a, cudaStream_t st) {
       const int64_t need = (a.g.ntiles + FAST_WARPS - 1) / FAST_WARPS;
       if (grid > need) grid = need;
       if (grid < 1) grid = 1;
-      DFastArgs fa{a, const_cast<unsigned int*>(a.redo_count), const_cast<long long*>(a.redo_list)};
       const bool t = g_timing.load(std::memory_order_relaxed);
       if (t) timing_mark(TK_DECOMPRESS, true, st);
       kern<<<(unsigned)grid, FAST_WARPS * 32, fsmem, st>>>(fa);
