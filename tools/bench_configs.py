@@ -68,6 +68,32 @@ def run(name, data, rel, b, pol, radius, reps=7):
         decomp()
     tc, kc = timed(comp, flush, reps)
     td, kd = timed(decomp, flush, reps)
+    # the same calls captured once into CUDA graphs (launch overhead removed;
+    # SURVEY 8d asks for this on the launch-bound small configs)
+    graphs = {}
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        comp()
+        decomp()
+    torch.cuda.current_stream().wait_stream(side)
+    for ph, fn in (("compress", comp), ("decompress", decomp)):
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr):
+            fn()
+        graphs[ph] = gr
+    tg = {}
+    for ph, gr in graphs.items():
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            gr.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        tg[ph] = statistics.median(ts)
     n = data.size
     alg = 6 * n + 4 * n_out + 8 * dev.grid.block_count
     print(json.dumps(dict(
@@ -75,6 +101,9 @@ def run(name, data, rel, b, pol, radius, reps=7):
         outliers=n_out, outlier_frac=n_out / n,
         compress_gbs=4 * n / tc / 1e6, decompress_gbs=4 * n / td / 1e6,
         compress_ms=tc, decompress_ms=td,
+        graph_compress_ms=tg["compress"], graph_decompress_ms=tg["decompress"],
+        graph_compress_gbs=4 * n / tg["compress"] / 1e6,
+        graph_decompress_gbs=4 * n / tg["decompress"] / 1e6,
         fused_compress_tbs=alg / (kc["compress"] * 1e-3) / 1e12 if kc["compress"] else None,
         fused_decompress_tbs=alg / (kd["decompress"] * 1e-3) / 1e12 if kd["decompress"] else None,
         kernels_compress=kc, kernels_decompress=kd)), flush=True)
