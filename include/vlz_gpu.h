@@ -195,7 +195,8 @@ int vlz_huff_encode_device(const uint16_t* d_codes, int64_t n, const void* d_tab
                            void* d_ws, size_t ws_bytes, void* stream);
 /* device decode (huffman.py:125-207 on the GPU, csrc/k_huffdec.cu):
  * self-synchronising parallel decode of the single MSB-first stream.
- * d_payload: 4-byte aligned device copy of the payload (nbytes).  Returns the
+ * d_payload: 4-byte aligned device copy of the payload (nbytes) followed by
+ * >= 16 zero bytes past nbytes rounded up to 4; d_out 16-byte aligned.  Returns the
  * same verdict codes as vlz_huff_decode (0 ok, 1..5) with *h_consumed, or a
  * negative VLZ_E_*; synchronises `stream`.  Code lengths <= 58. */
 size_t vlz_huff_decode_ws_size(int64_t nbytes);

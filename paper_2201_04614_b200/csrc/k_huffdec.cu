@@ -21,6 +21,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -33,16 +35,23 @@ namespace {
 
 constexpr int HD_S = 1024;        // bits per subsequence
 constexpr int HD_THREADS = 256;
-constexpr int HD_LBMAX = 11;      // table bits
+constexpr int HD_LBMAX = 12;      // table bits
 constexpr int HD_MAXLEN = 58;
 constexpr int HD_SCAN_IPT = 8;
 constexpr int HD_SCAN_CH = 256 * HD_SCAN_IPT;
 
 struct HDMeta {
   unsigned long long first_code[HD_MAXLEN + 2];
+  // first_code + count per length: past a table miss, the codeword length of
+  // a window is the smallest l whose l-bit prefix is below end[l] (canonical
+  // codes, huffman.py:33-45: prefixes of shorter codes come first)
+  unsigned long long end[HD_MAXLEN + 2];
   unsigned int first_idx[HD_MAXLEN + 2];
   unsigned int cnt[HD_MAXLEN + 2];
   unsigned int lut[1 << HD_LBMAX];  // sym << 8 | len (0: longer or invalid)
+  // counting passes: the codewords lying wholly inside a 12-bit window,
+  // (count << 4) | bits (0: the first codeword is longer than 12 bits)
+  unsigned char multi[1 << 12];
   int lb, maxlen;
 };
 
@@ -65,15 +74,10 @@ struct HDArgs {
   uint16_t* out;
 };
 
+// big-endian word w of the payload (the caller zero-pads 16 bytes past the
+// payload rounded up to 4 bytes; windows never reach further)
 __device__ __forceinline__ uint32_t ld_word(const HDArgs& a, int64_t w) {
-  const int64_t nw = (a.nbytes + 3) >> 2;
-  if (w >= nw) return 0u;
-  uint32_t x = a.words[w];
-  if (w == nw - 1 && (a.nbytes & 3)) {
-    const int keep = (int)(a.nbytes & 3);  // bytes in little-endian order
-    x &= (1u << (8 * keep)) - 1u;
-  }
-  return __byte_perm(x, 0, 0x0123);
+  return __byte_perm(__ldg(a.words + w), 0, 0x0123);
 }
 
 // up to 64 bits starting at bit p, left-aligned (bits past the payload = 0)
@@ -86,72 +90,102 @@ __device__ __forceinline__ unsigned long long peek64(const HDArgs& a, int64_t p)
 }
 
 // Decode the codewords of subsequence k that start in [start, lim).
-// WRITE: store symbols at out[o + j] for o + j < count.
+// Positions run relative to `start` in 32 bits (a subsequence spans HD_S bits
+// plus one codeword).  WRITE: store the symbols at out[o...] (only those with
+// index < count), eight at a time as one 16-byte store once aligned.
 template <bool WRITE>
 __device__ void decode_run(const HDArgs& a, const HDMeta& m, int64_t k, long long start,
                            long long o, long long& end, int& count_out, int& err_out) {
   const long long lim = (long long)(k + 1) * HD_S;
   const long long tb = a.total_bits;
-  long long pos = start;
-  int c = 0, err = 0;
+  const int stop = (int)((lim < tb ? lim : tb) - start);
+  // bits available from `start` (capped: only the last subsequence can run out)
+  const int avail = (int)((tb - start) < (long long)stop + 256 ? (tb - start) : stop + 256);
+  const int want = WRITE ? (int)((a.count - o) < (long long)HD_S ? (a.count - o) : HD_S) : HD_S;
+  int p = 0, c = 0, err = 0;
   const int LB = m.lb;
   // register bit window
-  int64_t wi = pos >> 5;
+  int64_t wi = start >> 5;
   unsigned long long buf = ((unsigned long long)ld_word(a, wi) << 32) | ld_word(a, wi + 1);
-  buf <<= (int)(pos & 31);
-  int nb = 64 - (int)(pos & 31);
+  buf <<= (int)(start & 31);
+  int nb = 64 - (int)(start & 31);
   wi += 2;
-  while (pos < lim && pos < tb) {
-    if (WRITE && o + c >= a.count) break;
+  // output packing (WRITE)
+  long long oi = o;
+  unsigned long long plo = 0, phi = 0;
+  int na = 0;
+  while (p < stop) {
+    if (WRITE && c >= want) break;
     if (nb < 32) {
       buf |= (unsigned long long)ld_word(a, wi) << (32 - nb);
       ++wi;
       nb += 32;
     }
+    if (!WRITE) {  // counting: every codeword inside the next 12 bits at once
+      const unsigned mt = m.multi[(unsigned)(buf >> 52)];
+      const int t = (int)(mt & 15u);
+      if (t != 0 && p + t <= stop && p + t <= avail) {
+        p += t;
+        c += (int)(mt >> 4);
+        buf <<= t;
+        nb -= t;
+        continue;
+      }
+    }
     const unsigned int ent = m.lut[(unsigned)(buf >> (64 - LB))];
     int len = (int)(ent & 0xffu);
-    unsigned sym;
-    if (len) {
-      sym = ent >> 8;
-    } else {
-      // canonical test for lengths LB+1 .. maxlen
-      const unsigned long long win = peek64(a, pos);
-      len = 0;
+    unsigned sym = ent >> 8;
+    if (len == 0) {
+      // longer codeword: the window holds >= 32 valid bits (a deeper book
+      // re-reads it); first length whose prefix lies below end[l]
+      const unsigned long long win = m.maxlen <= 32 ? buf : peek64(a, start + p);
       for (int l = LB + 1; l <= m.maxlen; ++l) {
         const unsigned long long code = win >> (64 - l);
-        if (code >= m.first_code[l] && code - m.first_code[l] < m.cnt[l]) {
+        if (code < m.end[l]) {
           len = l;
           sym = a.syms[m.first_idx[l] + (unsigned)(code - m.first_code[l])];
           break;
         }
       }
       if (len == 0) {  // no codeword: invalid prefix if maxlen+1 bits exist
-        if (tb - pos >= (long long)m.maxlen + 1) {
+        if (avail - p >= m.maxlen + 1) {
           err = 4;
-          pos += m.maxlen + 1;
+          p += m.maxlen + 1;
         } else {
           err = 3;
-          pos = tb;
+          p = avail;
         }
         break;
       }
     }
-    if (pos + len > tb) {  // the stream runs out mid-codeword
+    if (p + len > avail) {  // the stream runs out mid-codeword
       err = 3;
-      pos = tb;
+      p = avail;
       break;
     }
     if (WRITE) {
-      const long long idx = o + c;
-      a.out[idx] = (uint16_t)sym;
-      if (idx == a.count - 1) a.verdict[1] = pos + len;
+      if (oi == a.count - 1) a.verdict[1] = start + p + len;
+      if (na == 0 && (oi & 7)) {
+        a.out[oi] = (uint16_t)sym;
+      } else {
+        plo = (plo >> 16) | (phi << 48);
+        phi = (phi >> 16) | ((unsigned long long)sym << 48);
+        if (++na == 8) {
+          *reinterpret_cast<uint4*>(a.out + oi - 7) =
+              make_uint4((unsigned)plo, (unsigned)(plo >> 32), (unsigned)phi,
+                         (unsigned)(phi >> 32));
+          na = 0;
+        }
+      }
+      ++oi;
     }
-    pos += len;
+    p += len;
     ++c;
     if (len < nb) {
       buf <<= len;
       nb -= len;
     } else {  // long codeword: reload the window at the new position
+      const long long pos = start + p;
       wi = pos >> 5;
       buf = ((unsigned long long)ld_word(a, wi) << 32) | ld_word(a, wi + 1);
       buf <<= (int)(pos & 31);
@@ -159,7 +193,22 @@ __device__ void decode_run(const HDArgs& a, const HDMeta& m, int64_t k, long lon
       wi += 2;
     }
   }
-  end = pos;
+  if (WRITE && na) {  // the last < 8 packed symbols, oldest in the lowest bits
+    const int sh = 16 * (8 - na);
+    unsigned long long lo = plo, hi = phi;
+    if (sh >= 64) {
+      lo = hi >> (sh - 64);
+      hi = 0;
+    } else {
+      lo = (lo >> sh) | (hi << (64 - sh));
+      hi >>= sh;
+    }
+    for (int i = 0; i < na; ++i) {
+      const unsigned long long w = i < 4 ? lo >> (16 * i) : hi >> (16 * (i - 4));
+      a.out[oi - na + i] = (uint16_t)w;
+    }
+  }
+  end = start + p;
   count_out = c;
   err_out = err;
 }
@@ -317,7 +366,8 @@ int vlz_huff_decode_device(const uint8_t* d_payload, int64_t nbytes, int64_t bit
   if (count == 0) return bit_length != 0 ? 1 : 0;  // huffman.py order
   if (nbytes * 8 < bit_length) return 2;
   if (!d_out || !d_ws || (nbytes > 0 && !d_payload) ||
-      (reinterpret_cast<uintptr_t>(d_payload) & 3) || ws_bytes < vlz_huff_decode_ws_size(nbytes))
+      (reinterpret_cast<uintptr_t>(d_payload) & 3) || (reinterpret_cast<uintptr_t>(d_out) & 15) ||
+      ws_bytes < vlz_huff_decode_ws_size(nbytes))
     return VLZ_E_ARG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
 
@@ -337,6 +387,7 @@ int vlz_huff_decode_device(const uint8_t* d_payload, int64_t nbytes, int64_t bit
     for (int l = 1; l <= maxlen; ++l) {
       meta.first_code[l] = code;
       meta.first_idx[l] = idx;
+      meta.end[l] = code + meta.cnt[l];
       code = (code + meta.cnt[l]) << 1;
       idx += meta.cnt[l];
     }
@@ -356,6 +407,28 @@ int vlz_huff_decode_device(const uint8_t* d_payload, int64_t nbytes, int64_t bit
       }
       code += 1;
       if (i + 1 < nsym) code <<= (int)h_lens[i + 1] - L;
+    }
+    // 12-bit multi-codeword counts (greedy over a 12-bit first-codeword table)
+    std::vector<unsigned char> len12(4096, 0);
+    code = 0;
+    for (int i = 0; i < nsym; ++i) {
+      const int L = h_lens[i];
+      if (L <= 12) {
+        const unsigned long long b0 = code << (12 - L);
+        for (unsigned long long t = 0; t < (1ull << (12 - L)); ++t) len12[b0 + t] = (unsigned char)L;
+      }
+      code += 1;
+      if (i + 1 < nsym) code <<= (int)h_lens[i + 1] - L;
+    }
+    for (unsigned v = 0; v < 4096; ++v) {
+      int pos = 0, n = 0;
+      for (;;) {
+        const int L = len12[(v << pos) & 4095u];
+        if (L == 0 || pos + L > 12) break;
+        pos += L;
+        ++n;
+      }
+      meta.multi[v] = (unsigned char)((n << 4) | pos);
     }
   }
 
@@ -411,7 +484,9 @@ int vlz_huff_decode_device(const uint8_t* d_payload, int64_t nbytes, int64_t bit
         !ok(cudaStreamSynchronize(st)))
       return VLZ_E_CUDA;
     settled = changed == 0;
+    if (getenv("VLZ_HD_DEBUG")) fprintf(stderr, "hd: pass %d changed %u\n", it, changed);
   }
+  if (getenv("VLZ_HD_DEBUG")) fprintf(stderr, "hd: nsub %lld settled %d\n", (long long)nsub, (int)settled);
   if (!settled) {
     vlz::hd_chain_kernel<<<1, 32, 0, st>>>(a);
     vlz::g_launches.fetch_add(1, std::memory_order_relaxed);

@@ -74,6 +74,36 @@ def case(name, data, rel, b, pol, radius):
     assert int(info[0].item()) == nbits
     t_enc = ev_time(enc)
     t_hist = ev_time(hist)
+    # device decode of the same payload (includes its host-synchronised sync
+    # passes: wall time around the call, payload already on the device)
+    from paper_2201_04614_b200.huffman import decode_device
+
+    payload = out[: (nbits + 7) // 8].cpu().numpy().tobytes()
+    dec = decode_device(payload, nbits, cb, n)
+    assert torch.equal(dec, codes), "device decode mismatch"
+    dpay = torch.zeros((len(payload) + 3) // 4 * 4 + 16, dtype=torch.uint8, device="cuda")
+    dpay[: len(payload)].copy_(torch.frombuffer(bytearray(payload), dtype=torch.uint8))
+    dout = torch.empty(n, dtype=torch.int16, device="cuda")
+    dws = torch.empty(int(lib.vlz_huff_decode_ws_size(len(payload))), dtype=torch.uint8,
+                      device="cuda")
+    consumed = gpu.ctypes.c_int64(0)
+
+    def dec_call():
+        rc = lib.vlz_huff_decode_device(dpay.data_ptr(), len(payload), nbits, syms.ctypes.data,
+                                        lens.ctypes.data, len(syms), n, dout.data_ptr(),
+                                        gpu.ctypes.byref(consumed), dws.data_ptr(), dws.numel(),
+                                        None)
+        assert rc == 0
+
+    dec_call()
+    tds = []
+    for _ in range(5):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        dec_call()
+        torch.cuda.synchronize()
+        tds.append((time.perf_counter() - t0) * 1e3)
+    t_dec = statistics.median(tds)
     # full container pipeline (host array in, bytes out; and back)
     blob = vlzg.compress(data, cfg)
     t0 = time.perf_counter()
@@ -92,6 +122,7 @@ def case(name, data, rel, b, pol, radius):
         case=name, n=n, bits_per_symbol=nbits / n, nsym=len(syms), maxlen=int(lens.max()),
         encode_ms=t_enc, encode_gbs_codes=2 * n / t_enc / 1e6,
         encode_algorithmic_tbs=alg / t_enc / 1e9, histogram_ms=t_hist,
+        decode_ms=t_dec, decode_gbs_codes=2 * n / t_dec / 1e6,
         compress_pipeline_s=t_c, compress_pipeline_gbs=4 * n / t_c / 1e9,
         decompress_pipeline_s=t_d, decompress_pipeline_gbs=4 * n / t_d / 1e9,
         container_bytes=len(blob), ratio=4 * n / len(blob))), flush=True)
