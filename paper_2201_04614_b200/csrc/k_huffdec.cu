@@ -76,17 +76,19 @@ struct HDArgs {
 
 // big-endian word w of the payload (the caller zero-pads 16 bytes past the
 // payload rounded up to 4 bytes; windows never reach further)
-__device__ __forceinline__ uint32_t ld_word(const HDArgs& a, int64_t w) {
-  return __byte_perm(__ldg(a.words + w), 0, 0x0123);
+__device__ __forceinline__ uint32_t ld_word(const uint32_t* __restrict__ words, int64_t w) {
+  return __byte_perm(__ldg(words + w), 0, 0x0123);
 }
 
 // up to 64 bits starting at bit p, left-aligned (bits past the payload = 0)
-__device__ __forceinline__ unsigned long long peek64(const HDArgs& a, int64_t p) {
+__device__ __forceinline__ unsigned long long peek64(const uint32_t* __restrict__ words,
+                                                     int64_t p) {
   const int64_t w = p >> 5;
   const int off = (int)(p & 31);
-  const unsigned long long hi = ((unsigned long long)ld_word(a, w) << 32) | ld_word(a, w + 1);
+  const unsigned long long hi =
+      ((unsigned long long)ld_word(words, w) << 32) | ld_word(words, w + 1);
   if (off == 0) return hi;
-  return (hi << off) | ((unsigned long long)ld_word(a, w + 2) >> (32 - off));
+  return (hi << off) | ((unsigned long long)ld_word(words, w + 2) >> (32 - off));
 }
 
 // Decode the codewords of subsequence k that start in [start, lim).
@@ -96,17 +98,22 @@ __device__ __forceinline__ unsigned long long peek64(const HDArgs& a, int64_t p)
 template <bool WRITE>
 __device__ void decode_run(const HDArgs& a, const HDMeta& m, int64_t k, long long start,
                            long long o, long long& end, int& count_out, int& err_out) {
+  // kernel arguments into registers (the stores below cannot alias them)
+  const uint32_t* __restrict__ words = a.words;
+  const uint16_t* __restrict__ syms = a.syms;
+  uint16_t* __restrict__ out = a.out;
+  const long long count = a.count;
   const long long lim = (long long)(k + 1) * HD_S;
   const long long tb = a.total_bits;
   const int stop = (int)((lim < tb ? lim : tb) - start);
   // bits available from `start` (capped: only the last subsequence can run out)
   const int avail = (int)((tb - start) < (long long)stop + 256 ? (tb - start) : stop + 256);
-  const int want = WRITE ? (int)((a.count - o) < (long long)HD_S ? (a.count - o) : HD_S) : HD_S;
+  const int want = WRITE ? (int)((count - o) < (long long)HD_S ? (count - o) : HD_S) : HD_S;
   int p = 0, c = 0, err = 0;
   const int LB = m.lb;
   // register bit window
   int64_t wi = start >> 5;
-  unsigned long long buf = ((unsigned long long)ld_word(a, wi) << 32) | ld_word(a, wi + 1);
+  unsigned long long buf = ((unsigned long long)ld_word(words, wi) << 32) | ld_word(words, wi + 1);
   buf <<= (int)(start & 31);
   int nb = 64 - (int)(start & 31);
   wi += 2;
@@ -117,7 +124,7 @@ __device__ void decode_run(const HDArgs& a, const HDMeta& m, int64_t k, long lon
   while (p < stop) {
     if (WRITE && c >= want) break;
     if (nb < 32) {
-      buf |= (unsigned long long)ld_word(a, wi) << (32 - nb);
+      buf |= (unsigned long long)ld_word(words, wi) << (32 - nb);
       ++wi;
       nb += 32;
     }
@@ -138,12 +145,12 @@ __device__ void decode_run(const HDArgs& a, const HDMeta& m, int64_t k, long lon
     if (len == 0) {
       // longer codeword: the window holds >= 32 valid bits (a deeper book
       // re-reads it); first length whose prefix lies below end[l]
-      const unsigned long long win = m.maxlen <= 32 ? buf : peek64(a, start + p);
+      const unsigned long long win = m.maxlen <= 32 ? buf : peek64(words, start + p);
       for (int l = LB + 1; l <= m.maxlen; ++l) {
         const unsigned long long code = win >> (64 - l);
         if (code < m.end[l]) {
           len = l;
-          sym = a.syms[m.first_idx[l] + (unsigned)(code - m.first_code[l])];
+          sym = syms[m.first_idx[l] + (unsigned)(code - m.first_code[l])];
           break;
         }
       }
@@ -164,14 +171,13 @@ __device__ void decode_run(const HDArgs& a, const HDMeta& m, int64_t k, long lon
       break;
     }
     if (WRITE) {
-      if (oi == a.count - 1) a.verdict[1] = start + p + len;
       if (na == 0 && (oi & 7)) {
-        a.out[oi] = (uint16_t)sym;
+        out[oi] = (uint16_t)sym;
       } else {
         plo = (plo >> 16) | (phi << 48);
         phi = (phi >> 16) | ((unsigned long long)sym << 48);
         if (++na == 8) {
-          *reinterpret_cast<uint4*>(a.out + oi - 7) =
+          *reinterpret_cast<uint4*>(out + oi - 7) =
               make_uint4((unsigned)plo, (unsigned)(plo >> 32), (unsigned)phi,
                          (unsigned)(phi >> 32));
           na = 0;
@@ -187,7 +193,7 @@ __device__ void decode_run(const HDArgs& a, const HDMeta& m, int64_t k, long lon
     } else {  // long codeword: reload the window at the new position
       const long long pos = start + p;
       wi = pos >> 5;
-      buf = ((unsigned long long)ld_word(a, wi) << 32) | ld_word(a, wi + 1);
+      buf = ((unsigned long long)ld_word(words, wi) << 32) | ld_word(words, wi + 1);
       buf <<= (int)(pos & 31);
       nb = 64 - (int)(pos & 31);
       wi += 2;
@@ -205,9 +211,11 @@ __device__ void decode_run(const HDArgs& a, const HDMeta& m, int64_t k, long lon
     }
     for (int i = 0; i < na; ++i) {
       const unsigned long long w = i < 4 ? lo >> (16 * i) : hi >> (16 * (i - 4));
-      a.out[oi - na + i] = (uint16_t)w;
+      out[oi - na + i] = (uint16_t)w;
     }
   }
+  // the symbol `count` - 1 ends here: the reference's consumed bit count
+  if (WRITE && err == 0 && c == count - o) a.verdict[1] = start + p;
   end = start + p;
   count_out = c;
   err_out = err;
