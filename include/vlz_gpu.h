@@ -211,6 +211,12 @@ int vlz_huff_decode(const uint8_t* h_payload, int64_t nbytes, int64_t bit_length
                     const uint16_t* h_syms, const uint8_t* h_lens, int32_t nsym, int64_t count,
                     uint16_t* h_out, int64_t* h_consumed);
 
+/* border-outlier census (vector.py:82-87, collect_border): outliers (code 0)
+ * whose block-local coordinates include a 0, over a canonical uint16 code
+ * stream; *d_total (device int64) receives the count, stream-ordered */
+int vlz_border_outliers(const uint16_t* d_codes, const vlz_geom* g, int64_t* d_total,
+                        void* stream);
+
 /* number of kernel launches the library issued since load (bench evidence) */
 int64_t vlz_launch_count(void);
 /* per-kernel CUDA-event timing: when enabled every launch is bracketed by

@@ -68,6 +68,7 @@ PROTOTYPES = {
     "vlz_huff_build": (ctypes.c_int, [_vp, _vp, _vp, _P(ctypes.c_int32)]),
     "vlz_huff_encode": (ctypes.c_int, [_vp, _i64, _vp, _vp, ctypes.c_int32, _vp, _i64, _P(_i64),
                                        _P(_i64)]),
+    "vlz_border_outliers": (ctypes.c_int, [_vp, _P(Geom), _vp, _vp]),
     "vlz_huff_table_bytes": (ctypes.c_size_t, []),
     "vlz_huff_table": (ctypes.c_int, [_vp, _vp, ctypes.c_int32, _vp, _vp]),
     "vlz_huff_encode_ws_size": (ctypes.c_size_t, [_i64]),

@@ -306,5 +306,18 @@ def huffman_encode_device(codes: torch.Tensor, symbols: np.ndarray, lengths: np.
     return out[: (nb + 7) // 8].cpu().numpy().tobytes(), nb
 
 
+def border_outliers_device(codes: torch.Tensor, grid, stream=None) -> int:
+    """Outliers whose block-local coordinates include a 0 (vector.py:82-87),
+    counted on the device over a canonical uint16 (int16 storage) stream."""
+    lib = _lib.load()
+    c = codes.contiguous()
+    g = _lib.geom(grid.descriptor.dims, grid.block_edge)
+    total = torch.empty(1, dtype=torch.int64, device=c.device)
+    rc = lib.vlz_border_outliers(_ptr(c), ctypes.byref(g), _ptr(total), _stream(stream))
+    if rc != 0:
+        raise RuntimeError(f"vlz_border_outliers failed ({rc})")
+    return int(total.item())
+
+
 def launch_count() -> int:
     return int(_lib.load().vlz_launch_count())

@@ -49,7 +49,8 @@ def to_codestream(dev: gpu.DeviceCodeStream) -> CodeStream:
 
 
 def border_outliers(stream: CodeStream) -> int:
-    """Outliers whose block-local coordinates include a 0 (vector.py:82-87)."""
+    """Outliers whose block-local coordinates include a 0 (vector.py:82-87),
+    from a host CodeStream (the GPU path uses gpu.border_outliers_device)."""
     grid = stream.grid
     dims = grid.descriptor.dims
     nd = len(dims)
@@ -108,5 +109,6 @@ def dualquant(data: np.ndarray, config: CompressionConfig, collect_border: bool 
     stream = to_codestream(out)
     if collect_border:
         total = int(stream.outlier_counts.sum())
-        return stream, (total, border_outliers(stream))
+        border = gpu.border_outliers_device(out.codes[: desc.element_count], stream.grid)
+        return stream, (total, border)
     return stream

@@ -48,6 +48,15 @@ def load_json(name: str):
         return json.load(fh)
 
 
+def load_border():
+    """border.npz: outlier_report rows from the reference (make_golden.make_border)."""
+    z = np.load(os.path.join(GOLDEN, "border.npz"))
+    cases = json.loads(bytes(z["meta"]))
+    for c in cases:
+        c["data"] = np.frombuffer(bytes.fromhex(c["data"]), dtype=np.float32).reshape(c["shape"])
+    return cases
+
+
 @pytest.fixture(scope="session")
 def corpus_cases():
     return load_cases("corpus.npz")

@@ -21,6 +21,8 @@ Fixture groups
   known.json      hand known-answer cases lifted from the reference tests.
   fullsize.json   sha256 of the reference streams for C1/C2 at full size
                   (regenerated data via paper_2201_04614_b200.workloads).
+  border.npz      outlier_report rows (total / border outliers per padding
+                  policy, reduction vs zero padding) for seeded arrays.
 """
 
 from __future__ import annotations
@@ -441,7 +443,37 @@ def make_fullsize():
     print("wrote fullsize.json")
 
 
+def make_border():
+    """outlier_report (padding.py:162-205): per-policy total / border outlier
+    counts and the reduction versus zero padding, from the reference."""
+    from vlz.padding import outlier_report
+
+    cases = []
+    rng = np.random.default_rng(23)
+    shapes = [(200,), (37, 41), (19, 23, 29), (16, 16, 16), (9, 40, 33)]
+    for k, shape in enumerate(shapes):
+        for b in (8, 16):
+            if len(shape) == 1 and b == 16:
+                continue
+            data = (_smooth(rng, shape) + 0.003 * _noise(rng, shape)).astype(np.float32)
+            eb = float(0.002 * (float(data.max()) - float(data.min())))
+            for radius in (8, 512):
+                cfg = _cfg(eb, b, "zero", radius)
+                rows = outlier_report(data, cfg)
+                cases.append(dict(
+                    tag=f"border{k}_b{b}_r{radius}", shape=list(shape),
+                    data=data.tobytes().hex(), eb=eb, block_edge=b, radius=radius,
+                    rows=[dict(kind=r.policy.value_kind.value, gran=r.policy.granularity.value,
+                               total=r.total_outliers, border=r.border_outliers,
+                               reduction=red) for r, red in rows]))
+    blob = json.dumps(cases).encode()
+    np.savez_compressed(os.path.join(HERE, "border.npz"),
+                        meta=np.frombuffer(blob, dtype=np.uint8))
+    print(f"wrote border.npz: {len(cases)} cases")
+
+
 if __name__ == "__main__":
-    what = sys.argv[1:] or ["corpus", "errors", "corrupt", "known", "fullsize", "container"]
+    what = sys.argv[1:] or ["corpus", "errors", "corrupt", "known", "fullsize", "container",
+                            "border"]
     for w in what:
         globals()[f"make_{w}"]()

@@ -241,3 +241,17 @@ def test_fast_kernel_edge_tiles(oracle, shape, b):
     for eb, pol in ((1e-3, "mean:global"), (1e-4, "zero"), (1e-3, "max:block")):
         s = _check_full(oracle, data, eb, b, pol, 512)
         assert s.outlier_values.size > 0
+
+
+def test_outlier_report_matches_reference():
+    # padding.py:162-205 on the GPU (border census: csrc/k_stats.cu)
+    from conftest import load_border
+    from paper_2201_04614_b200.padding import outlier_report
+
+    for c in load_border():
+        cfg = _cfg(c["eb"], c["block_edge"], "zero", c["radius"])
+        rows = outlier_report(c["data"], cfg)
+        got = [dict(kind=r.policy.value_kind.value, gran=r.policy.granularity.value,
+                    total=r.total_outliers, border=r.border_outliers, reduction=red)
+               for r, red in rows]
+        assert got == c["rows"], c["tag"]

@@ -111,3 +111,26 @@ def test_oracle_fullsize_reference_hashes(oracle):
         assert _sha(got["outlier_values"]) == c["outliers_sha"]
         assert _sha(got["outlier_counts"]) == c["counts_sha"]
         assert _sha(got["scalars"]) == c["scalars_sha"]
+
+
+def test_oracle_border_census_matches_reference_outlier_report(oracle):
+    # padding.py:162-205 / vector.py:82-87: total and border outliers per
+    # policy, from the pinned oracle's stream through the host census
+    from types import SimpleNamespace
+
+    from conftest import load_border
+    from paper_2201_04614_b200 import model as M
+    from paper_2201_04614_b200.vector import border_outliers
+
+    n = 0
+    for c in load_border():
+        grid = M.build_block_grid(M.ArrayDescriptor(len(c["shape"]), tuple(c["shape"])),
+                                  c["block_edge"])
+        for row in c["rows"]:
+            pol = f"{row['kind']}:{row['gran']}" if row["kind"] != "zero" else "zero"
+            o = oracle.dualquant(c["data"], c["eb"], c["block_edge"], c["radius"], pol)
+            assert int(o["outlier_counts"].sum()) == row["total"], (c["tag"], pol)
+            s = SimpleNamespace(grid=grid, codes=o["codes"])
+            assert border_outliers(s) == row["border"], (c["tag"], pol)
+            n += 1
+    assert n >= 150
