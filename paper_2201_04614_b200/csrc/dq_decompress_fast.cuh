@@ -465,8 +465,8 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, 4)
     dq_decompress_tma_kernel(const __grid_constant__ DFastArgs fa) {
   using T = DTmaShape<ND, B, VPL>;
   extern __shared__ __align__(1024) unsigned char smem_dtma[];
-  unsigned char* base = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_dtma) + 1023) & ~uintptr_t(1023));
+  // align by an offset from the shared array itself (keeps the accesses LDS/STS)
+  unsigned char* base = smem_dtma + ((1024u - (smem_u32(smem_dtma) & 1023u)) & 1023u);
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   unsigned char* ring = base + (size_t)wib * T::WARP_SMEM;
