@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(HE_THREADS, 3) huff_encode_kernel(HEArgs a) {
     for (int q = 0; q < HE_SPT / 8; ++q) pk[q] = make_uint4(0, 0, 0, 0);
   }
   unsigned long long tail_e = 0;
-  const bool need_tail_sym = (wid == 0) && (base + HE_CH < a.n);
+  const bool need_tail_sym = (wid == 1) && (base + HE_CH < a.n);
   if (need_tail_sym) {
     const int64_t i = base + HE_CH + lane;
     if (i < a.n) tail_e = __ldg(a.tab + a.codes[i]);
@@ -147,27 +147,18 @@ __global__ void __launch_bounds__(HE_THREADS, 3) huff_encode_kernel(HEArgs a) {
     agg += s_warp[w];
   }
   const int texcl = wbase + inc - tbits;
-  if (wid == 0) {
-    const long long excl = lookback_exclusive(a.lb, tile, agg, lane);
-    if (lane == 0) {
-      s_start = excl;
-      if (base + HE_CH >= a.n) a.info[0] = excl + agg;
-    }
-  }
-  __syncthreads();
-  const long long start = s_start;
-  const int sh = (int)(start & 31);
-  const int e_local = sh + agg;
-  const int nwords = (e_local + 31) / 32;
+  // the chunk's bits are assembled at LOCAL offsets (bit 0 = the chunk's
+  // first bit), so only the final store waits for the look-back; the next
+  // chunk's leading <= 32 bits are appended after them
+  const int nwords = (agg + 32 + 31) / 32 + 1;
   for (int w = tid; w < nwords; w += HE_THREADS) s_words[w] = 0;
   __syncthreads();
 
-  // ---- assemble this chunk's bits (aligned to the global word grid): a
-  // 64-bit accumulator per thread; words wholly inside the thread's bit range
-  // are plain shared stores, the (at most two) words shared with the
-  // neighbouring threads are atomicOr
-  {
-    const int p0 = sh + texcl;
+  auto compose = [&]() {
+    // 64-bit accumulator per thread; words wholly inside the thread's bit
+    // range are plain shared stores, the (at most two) words shared with the
+    // neighbouring threads are atomicOr
+    const int p0 = texcl;
     int w = p0 >> 5;
     int nacc = p0 & 31;  // leading zero bits of the first word
     unsigned long long acc = 0;
@@ -199,32 +190,51 @@ __global__ void __launch_bounds__(HE_THREADS, 3) huff_encode_kernel(HEArgs a) {
       }
     }
     if (nacc > (first ? (p0 & 31) : 0)) atomicOr(&s_words[w], (uint32_t)(acc << (32 - nacc)));
-  }
-  // ---- complete the last (shared) word from the next chunk's leading symbols
-  if (need_tail_sym && (e_local & 31)) {
-    const int L = (int)(tail_e & 63);
-    int x = L;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int u = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += u;
+  };
+
+  if (wid == 0) {  // look-back first, then this warp's share of the bits
+    const long long excl = lookback_exclusive(a.lb, tile, agg, lane);
+    if (lane == 0) {
+      s_start = excl;
+      if (base + HE_CH >= a.n) a.info[0] = excl + agg;
     }
-    const int excl = x - L;
-    const int need = 32 - (e_local & 31);
-    if (L > 0 && excl < need) {
-      const int take = L < need - excl ? L : need - excl;
-      const uint32_t bits = (uint32_t)(((tail_e >> 6) << (64 - L)) >> (64 - take));
-      const int o = (e_local + excl) & 31;
-      atomicOr(&s_words[e_local >> 5], bits << (32 - o - take));
+    compose();
+  } else {
+    compose();
+    if (wid == 1 && base + HE_CH < a.n) {
+      // the next chunk's leading bits, 32 of them, at local [agg, agg + 32)
+      // (every codeword has >= 1 bit, so 32 symbols always suffice)
+      const int L = (int)(tail_e & 63);
+      int x = L;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += u;
+      }
+      const int excl = x - L;
+      if (L > 0 && excl < 32) {
+        const int take = L < 32 - excl ? L : 32 - excl;
+        const unsigned long long bits =
+            (((tail_e >> 6) << (64 - L)) >> (64 - take)) << (64 - take);  // left-aligned
+        const int p = agg + excl;
+        const unsigned long long y = bits >> (p & 31);
+        atomicOr(&s_words[p >> 5], (uint32_t)(y >> 32));
+        if ((uint32_t)y) atomicOr(&s_words[(p >> 5) + 1], (uint32_t)y);
+      }
     }
   }
   __syncthreads();
 
-  // ---- store the owned words (first bit inside [start, start + agg))
+  // ---- store the owned words (first bit inside [start, start + agg)): output
+  // word gw holds local bits [32 gw - start, +32), a funnel of two local words
+  const long long start = s_start;
+  const int sh = (int)(start & 31);
   const int64_t gw0 = start >> 5;
-  for (int lw = (sh ? 1 : 0) + tid; lw < nwords; lw += HE_THREADS) {
-    const int64_t gw = gw0 + lw;
-    if (gw < a.out_words) a.out[gw] = __byte_perm(s_words[lw], 0, 0x0123);
+  const int nout = (sh + agg + 31) / 32;
+  for (int m = (sh ? 1 : 0) + tid; m < nout; m += HE_THREADS) {
+    const uint32_t word = sh ? __funnelshift_r(s_words[m], s_words[m - 1], sh) : s_words[m];
+    const int64_t gw = gw0 + m;
+    if (gw < a.out_words) a.out[gw] = __byte_perm(word, 0, 0x0123);
     else a.info[2] = 1;
   }
 }
@@ -299,11 +309,11 @@ int vlz_huff_encode_device(const uint16_t* d_codes, int64_t n, const void* d_tab
   a.ticket = ticket;
   a.info = reinterpret_cast<long long*>(d_info);
   // shared words: the chunk's bits at max_len per symbol, plus alignment
-  const size_t smem = ((size_t)vlz::HE_CH * max_len / 32 + 2) * 4;
+  const size_t smem = ((size_t)vlz::HE_CH * max_len / 32 + 4) * 4;
   static bool attr_set = false;  // opt in to > 48 KB once (up to 58-bit books)
   if (!attr_set) {
     if (cudaFuncSetAttribute(vlz::huff_encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             ((size_t)vlz::HE_CH * vlz::HE_MAXLEN / 32 + 2) * 4) != cudaSuccess)
+                             ((size_t)vlz::HE_CH * vlz::HE_MAXLEN / 32 + 4) * 4) != cudaSuccess)
       return VLZ_E_CUDA;
     attr_set = true;
   }
