@@ -82,7 +82,7 @@ __device__ __forceinline__ unsigned sym_at(const uint4* pk, int k) {
   return (k & 1) ? (x >> 16) : (x & 0xffffu);
 }
 
-__global__ void __launch_bounds__(HE_THREADS, 3) huff_encode_kernel(HEArgs a) {
+__global__ void __launch_bounds__(HE_THREADS, 4) huff_encode_kernel(HEArgs a) {
   extern __shared__ uint32_t s_words[];  // sized for HE_CH * max_len bits
   __shared__ int s_warp[HE_THREADS / 32];
   __shared__ long long s_start;
@@ -119,17 +119,26 @@ __global__ void __launch_bounds__(HE_THREADS, 3) huff_encode_kernel(HEArgs a) {
 
   // ---- lengths -> bits of this thread
   int tbits = 0;
+  int lmin = 64, lmax = 0;
 #pragma unroll
   for (int k = 0; k < HE_SPT; ++k) {
     const int s = sym_of(k);
     if (s < 0) continue;
     const int L = __ldg(a.len + s);
-    if (L == 0) {  // not in the codebook (reported, contributes no bits)
-      const long long tag = ((i0 + k) << 16) | (long long)s;
-      atomicMin(&a.info[s >= a.nsym_span ? 1 : 3], tag);
-    }
+    lmin = min(lmin, L);
+    lmax = max(lmax, L);
     tbits += L;
   }
+  if (lmin == 0) {  // symbols not in the codebook (reported, contribute no bits)
+#pragma unroll 1
+    for (int k = 0; k < HE_SPT; ++k) {
+      const int s = sym_of(k);
+      if (s >= 0 && __ldg(a.len + s) == 0)
+        atomicMin(&a.info[s >= a.nsym_span ? 1 : 3], ((i0 + k) << 16) | (long long)s);
+    }
+  }
+  // common case: every symbol present, every codeword <= 32 bits
+  const bool simple = full && lmin > 0 && lmax <= 32;
 
   // ---- chunk scan of bit lengths
   int inc = tbits;
@@ -155,6 +164,30 @@ __global__ void __launch_bounds__(HE_THREADS, 3) huff_encode_kernel(HEArgs a) {
   __syncthreads();
 
   auto compose = [&]() {
+    if (simple) {  // branch-light path: every codeword 1..32 bits
+      const int p0 = texcl;
+      int w = p0 >> 5;
+      int nacc = p0 & 31;
+      unsigned long long acc = 0;
+      int emitted = 0;
+#pragma unroll
+      for (int k = 0; k < HE_SPT; ++k) {
+        const unsigned long long e = __ldg(a.tab + sym_at(pk, k));
+        const int L = (int)(e & 63);
+        acc = (acc << L) | (e >> 6);
+        nacc += L;
+        if (nacc >= 32) {
+          const uint32_t word = (uint32_t)(acc >> (nacc - 32));
+          nacc -= 32;
+          if (emitted == 0) atomicOr(&s_words[w], word);
+          else s_words[w] = word;
+          ++emitted;
+          ++w;
+        }
+      }
+      if (nacc > (emitted ? 0 : (p0 & 31))) atomicOr(&s_words[w], (uint32_t)(acc << (32 - nacc)));
+      return;
+    }
     // 64-bit accumulator per thread; words wholly inside the thread's bit
     // range are plain shared stores, the (at most two) words shared with the
     // neighbouring threads are atomicOr
