@@ -21,8 +21,6 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
-#include <cstdio>
-#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -492,9 +490,7 @@ int vlz_huff_decode_device(const uint8_t* d_payload, int64_t nbytes, int64_t bit
         !ok(cudaStreamSynchronize(st)))
       return VLZ_E_CUDA;
     settled = changed == 0;
-    if (getenv("VLZ_HD_DEBUG")) fprintf(stderr, "hd: pass %d changed %u\n", it, changed);
   }
-  if (getenv("VLZ_HD_DEBUG")) fprintf(stderr, "hd: nsub %lld settled %d\n", (long long)nsub, (int)settled);
   if (!settled) {
     vlz::hd_chain_kernel<<<1, 32, 0, st>>>(a);
     vlz::g_launches.fetch_add(1, std::memory_order_relaxed);

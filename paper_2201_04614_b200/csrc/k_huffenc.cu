@@ -343,13 +343,10 @@ int vlz_huff_encode_device(const uint16_t* d_codes, int64_t n, const void* d_tab
   a.info = reinterpret_cast<long long*>(d_info);
   // shared words: the chunk's bits at max_len per symbol, plus alignment
   const size_t smem = ((size_t)vlz::HE_CH * max_len / 32 + 4) * 4;
-  static bool attr_set = false;  // opt in to > 48 KB once (up to 58-bit books)
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(vlz::huff_encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             ((size_t)vlz::HE_CH * vlz::HE_MAXLEN / 32 + 4) * 4) != cudaSuccess)
-      return VLZ_E_CUDA;
-    attr_set = true;
-  }
+  // opt in to > 48 KB (books up to 58 bits); per device, so set every call
+  if (cudaFuncSetAttribute(vlz::huff_encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           ((size_t)vlz::HE_CH * vlz::HE_MAXLEN / 32 + 4) * 4) != cudaSuccess)
+    return VLZ_E_CUDA;
   vlz::huff_encode_kernel<<<(unsigned)nchunks, vlz::HE_THREADS, smem, st>>>(a);
   vlz::g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError() == cudaSuccess ? VLZ_OK : VLZ_E_CUDA;
