@@ -14,8 +14,10 @@
 //  4. write pass: re-decode, store symbols with index < count, and settle
 //     the verdict: the first subsequence (in stream order) that reaches
 //     `count` or stops on an error decides it.
-// Decoding: a 2^LB-entry (symbol, length) table in shared memory for
-// codewords up to LB <= 11 bits; longer ones by the canonical first-code
+// Decoding: a 4096-entry table in shared memory over the next 12 bits gives
+// the first one or two codewords (symbols and lengths) when they fit, and a
+// second 4096-entry table the number of codewords inside the 12 bits for the
+// counting passes; longer codewords take the canonical first-code
 // test per length (huffman.py:33-45 ordering).  The bit window is a 64-bit
 // register refilled 32 bits at a time from big-endian words.
 #include <cuda_runtime.h>
@@ -33,7 +35,6 @@ namespace {
 
 constexpr int HD_S = 1024;        // bits per subsequence
 constexpr int HD_THREADS = 256;
-constexpr int HD_LBMAX = 12;      // table bits
 constexpr int HD_MAXLEN = 58;
 constexpr int HD_SCAN_IPT = 8;
 constexpr int HD_SCAN_CH = 256 * HD_SCAN_IPT;
@@ -46,11 +47,14 @@ struct HDMeta {
   unsigned long long end[HD_MAXLEN + 2];
   unsigned int first_idx[HD_MAXLEN + 2];
   unsigned int cnt[HD_MAXLEN + 2];
-  unsigned int lut[1 << HD_LBMAX];  // sym << 8 | len (0: longer or invalid)
+  // first codewords inside a 12-bit window: bits 0-1 count (0: the first is
+  // longer than 12 bits or invalid), 2-5 first length, 6-9 first + second
+  // length, 16-31 first symbol, 32-47 second symbol
+  unsigned long long pair[1 << 12];
   // counting passes: the codewords lying wholly inside a 12-bit window,
   // (count << 4) | bits (0: the first codeword is longer than 12 bits)
   unsigned char multi[1 << 12];
-  int lb, maxlen;
+  int maxlen;
 };
 
 struct HDArgs {
@@ -108,7 +112,6 @@ __device__ void decode_run(const HDArgs& a, const HDMeta& m, int64_t k, long lon
   const int avail = (int)((tb - start) < (long long)stop + 256 ? (tb - start) : stop + 256);
   const int want = WRITE ? (int)((count - o) < (long long)HD_S ? (count - o) : HD_S) : HD_S;
   int p = 0, c = 0, err = 0;
-  const int LB = m.lb;
   // register bit window
   int64_t wi = start >> 5;
   unsigned long long buf = ((unsigned long long)ld_word(words, wi) << 32) | ld_word(words, wi + 1);
@@ -137,14 +140,43 @@ __device__ void decode_run(const HDArgs& a, const HDMeta& m, int64_t k, long lon
         continue;
       }
     }
-    const unsigned int ent = m.lut[(unsigned)(buf >> (64 - LB))];
-    int len = (int)(ent & 0xffu);
-    unsigned sym = ent >> 8;
-    if (len == 0) {
+    const unsigned long long ent = m.pair[(unsigned)(buf >> 52)];
+    int len = (int)((ent >> 2) & 15u);
+    unsigned sym = (unsigned)(ent >> 16) & 0xffffu;
+    if (WRITE && (ent & 3u) == 2u) {  // two codewords at once when both fit
+      const int len2 = (int)((ent >> 6) & 15u);
+      if (p + len < stop && p + len2 <= avail && c + 2 <= want) {
+        const unsigned sym2 = (unsigned)(ent >> 32) & 0xffffu;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const unsigned sq = q ? sym2 : sym;
+          if (na == 0 && (oi & 7)) {
+            out[oi] = (uint16_t)sq;
+          } else {
+            plo = (plo >> 16) | (phi << 48);
+            phi = (phi >> 16) | ((unsigned long long)sq << 48);
+            if (++na == 8) {
+              *reinterpret_cast<uint4*>(out + oi - 7) =
+                  make_uint4((unsigned)plo, (unsigned)(plo >> 32), (unsigned)phi,
+                             (unsigned)(phi >> 32));
+              na = 0;
+            }
+          }
+          ++oi;
+        }
+        p += len2;
+        c += 2;
+        buf <<= len2;
+        nb -= len2;
+        continue;
+      }
+    }
+    if ((ent & 3u) == 0u) {
       // longer codeword: the window holds >= 32 valid bits (a deeper book
       // re-reads it); first length whose prefix lies below end[l]
       const unsigned long long win = m.maxlen <= 32 ? buf : peek64(words, start + p);
-      for (int l = LB + 1; l <= m.maxlen; ++l) {
+      len = 0;
+      for (int l = 13; l <= m.maxlen; ++l) {
         const unsigned long long code = win >> (64 - l);
         if (code < m.end[l]) {
           len = l;
@@ -398,33 +430,37 @@ int vlz_huff_decode_device(const uint8_t* d_payload, int64_t nbytes, int64_t bit
       idx += meta.cnt[l];
     }
   }
-  const int lb = maxlen < vlz::HD_LBMAX ? maxlen : vlz::HD_LBMAX;
-  meta.lb = lb;
   meta.maxlen = maxlen;
   {
-    unsigned long long code = 0;
-    for (int i = 0; i < nsym; ++i) {
-      const int L = h_lens[i];
-      if (L <= lb) {
-        const unsigned long long b0 = code << (lb - L);
-        const unsigned long long span = 1ull << (lb - L);
-        for (unsigned long long t = 0; t < span; ++t)
-          meta.lut[b0 + t] = ((unsigned)h_syms[i] << 8) | (unsigned)L;
-      }
-      code += 1;
-      if (i + 1 < nsym) code <<= (int)h_lens[i + 1] - L;
-    }
-    // 12-bit multi-codeword counts (greedy over a 12-bit first-codeword table)
+    // first codeword of every 12-bit window (codewords up to 12 bits)
     std::vector<unsigned char> len12(4096, 0);
-    code = 0;
+    std::vector<uint16_t> sym12(4096, 0);
+    unsigned long long code = 0;
     for (int i = 0; i < nsym; ++i) {
       const int L = h_lens[i];
       if (L <= 12) {
         const unsigned long long b0 = code << (12 - L);
-        for (unsigned long long t = 0; t < (1ull << (12 - L)); ++t) len12[b0 + t] = (unsigned char)L;
+        for (unsigned long long t = 0; t < (1ull << (12 - L)); ++t) {
+          len12[b0 + t] = (unsigned char)L;
+          sym12[b0 + t] = h_syms[i];
+        }
       }
       code += 1;
       if (i + 1 < nsym) code <<= (int)h_lens[i + 1] - L;
+    }
+    for (unsigned v = 0; v < 4096; ++v) {
+      const int L1 = len12[v];
+      unsigned long long e = 0;
+      if (L1) {
+        e = 1u | ((unsigned long long)L1 << 2) | ((unsigned long long)L1 << 6) |
+            ((unsigned long long)sym12[v] << 16);
+        const int L2 = len12[(v << L1) & 4095u];
+        if (L2 && L1 + L2 <= 12)
+          e = 2u | ((unsigned long long)L1 << 2) | ((unsigned long long)(L1 + L2) << 6) |
+              ((unsigned long long)sym12[v] << 16) |
+              ((unsigned long long)sym12[(v << L1) & 4095u] << 32);
+      }
+      meta.pair[v] = e;
     }
     for (unsigned v = 0; v < 4096; ++v) {
       int pos = 0, n = 0;
