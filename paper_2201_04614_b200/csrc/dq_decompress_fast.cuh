@@ -16,11 +16,12 @@
 //    congruence mod 2^32 is equality.  The kernel checks exactly that and
 //    hands any tile that fails it to the int64 kernel
 //    (dq_decompress_kernel<..., LIST=true>);
-//  * edge tiles (partial last block row / window) run afterwards in
-//    dq_decompress_edge_kernel, the same recurrence instantiated with EDGE:
-//    codes are fetched synchronously (partial blocks are not 4-byte aligned)
-//    and positions beyond the array read as "delta 0" -- they trail every
-//    valid position of their block in x and y, so they never feed one;
+//  * edge tiles (partial last block row / window) run inline in grids that
+//    have them (EDGES variants), the same recurrence instantiated with EDGE:
+//    codes are fetched synchronously into a slot of their own (partial blocks
+//    are not 4-byte aligned) and positions beyond the array read as "delta 0"
+//    -- they trail every valid position of their block in x and y, so they
+//    never feed one;
 //  * output rows leave with 16-byte stores straight from registers; rows are
 //    unrolled by two so that the dequantisation of one row overlaps the
 //    scans of the next;
@@ -43,7 +44,10 @@ struct DFastShape {
   static constexpr int LANE_BYTES = VPL * 2;
   static constexpr int STAGE_BYTES = S::BY * 32 * LANE_BYTES;
   static constexpr int PREV_BYTES = (ND == 3) ? S::BY * S::W * 4 : 0;
-  static constexpr int WARP_SMEM = FAST_STAGES * STAGE_BYTES + PREV_BYTES;
+  // edge tiles fill their codes synchronously into a slot of their own, so
+  // the ring of interior planes keeps streaming underneath
+  static constexpr int EDGE_OFF = FAST_STAGES * STAGE_BYTES + PREV_BYTES;
+  static constexpr int WARP_SMEM = EDGE_OFF + STAGE_BYTES;
 };
 
 template <int ND, int B, int VPL>
@@ -225,7 +229,7 @@ __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, c
   bool badcode = false;
   int dmax = 0, dmin = 0;  // range of every d of the tile (exact iff within +-2^27)
   float* orow = a.out + (z0 * g.D1 + y0) * g.D2 + xl0;
-  const unsigned char* const slot0 = ring + lane * F::LANE_BYTES;
+  const unsigned char* const slot0 = ring + (EDGE ? F::EDGE_OFF : 0) + lane * F::LANE_BYTES;
 
   const uint16_t* esrc = nullptr;
   if (EDGE) esrc = codes + block_start(g, tc.bz, tc.by, bxg, BZ, BY, BX, ez, ey) + xin;
@@ -233,7 +237,7 @@ __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, c
     const unsigned char* slot;
     if (EDGE) {
       // synchronous fill of stage 0: invalid positions read as code R
-      unsigned char* fill = ring + lane * F::LANE_BYTES;
+      unsigned char* fill = ring + F::EDGE_OFF + lane * F::LANE_BYTES;
       const uint16_t* zs = esrc + (int64_t)zl * ey * ex;
 #pragma unroll
       for (int yl = 0; yl < BY; ++yl) {
@@ -264,7 +268,7 @@ __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, c
     for (int yl = 0; yl < ey; ++yl) {
       unsigned c[VPL];
       const unsigned char* rowp = slot;
-      if (TMAP)  // block blk, row yl: 16-byte chunk yl of line blk, XOR-swizzled
+      if (TMAP && !EDGE)  // block blk, row yl: 16-byte chunk yl of line blk, XOR-swizzled
         rowp = slot + blk * 128 + (((yl ^ blk) & 7) << 4) + (xin * 2);
       if (VPL == 4) {
         const uint2 pk = *reinterpret_cast<const uint2*>(rowp);
@@ -274,7 +278,7 @@ __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, c
         const unsigned pk = *reinterpret_cast<const unsigned*>(rowp);
         c[0] = pk & 0xffffu; c[1 % VPL] = pk >> 16;
       }
-      if (!TMAP) slot += 32 * F::LANE_BYTES;
+      if (!TMAP || EDGE) slot += 32 * F::LANE_BYTES;
       int ep[VPL];
       if (ND == 3) {
         if (VPL == 4) {
@@ -393,12 +397,12 @@ __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, c
       dst += g.D2;
     }
     orow += g.D1 * g.D2;
-    if constexpr (TMAP) {
+    if constexpr (TMAP && !EDGE) {
       __syncwarp();
       fence_proxy_async_smem();
       prod.issue(g, &fa.tmap, ring, bars, lane, nwarps);
       cons.advance();
-    } else if (!EDGE) {
+    } else if constexpr (!EDGE && !TMAP) {
       prod.issue(g, codes, ring, nwarps, lane);
       cons.advance();
     }
@@ -419,7 +423,10 @@ __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, c
   }
 }
 
-template <int ND, int B, int VPL>
+// EDGES: the grid has edge tiles (processed inline, at the cost of the
+// registers of a second instantiation of the tile body); grids without them
+// take the lean variant
+template <int ND, int B, int VPL, bool EDGES>
 __global__ void __launch_bounds__(FAST_WARPS * 32, 4)
     dq_decompress_fast_kernel(const __grid_constant__ DFastArgs fa) {
   using F = DFastShape<ND, B, VPL>;
@@ -439,8 +446,10 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, 4)
   long long sent = 0;
   for (uint32_t tile = first; tile < (uint32_t)g.ntiles; tile += nwarps) {
     const TileXY tc = decode_tile(g, tile);
-    if (!tile_interior<ND, B, VPL>(g, tc)) continue;  // dq_decompress_edge_kernel
-    dfast_tile<ND, B, VPL, false>(fa, tile, tc, lane, ring, nullptr, prod, cons, nwarps, sent);
+    if (tile_interior<ND, B, VPL>(g, tc))
+      dfast_tile<ND, B, VPL, false>(fa, tile, tc, lane, ring, nullptr, prod, cons, nwarps, sent);
+    else if constexpr (EDGES)  // same recurrence, synchronous fill (the ring keeps streaming)
+      dfast_tile<ND, B, VPL, true>(fa, tile, tc, lane, ring, nullptr, prod, cons, nwarps, sent);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) sent += __shfl_xor_sync(FULL, sent, o);
@@ -452,7 +461,7 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, 4)
 template <int ND, int B, int VPL>
 struct DTmaShape {
   using F = DFastShape<ND, B, VPL>;
-  static constexpr int BAR_OFF = FAST_STAGES * F::STAGE_BYTES + F::PREV_BYTES;
+  static constexpr int BAR_OFF = F::WARP_SMEM;  // stages | previous plane | edge slot
   static constexpr int WARP_SMEM = (BAR_OFF + 64 + 1023) / 1024 * 1024;
 };
 template <int ND, int B, int VPL>
@@ -460,7 +469,7 @@ __host__ __device__ constexpr int dtma_smem_bytes() {
   return FAST_WARPS * DTmaShape<ND, B, VPL>::WARP_SMEM + 1024;
 }
 
-template <int ND, int B, int VPL>
+template <int ND, int B, int VPL, bool EDGES>
 __global__ void __launch_bounds__(FAST_WARPS * 32, 4)
     dq_decompress_tma_kernel(const __grid_constant__ DFastArgs fa) {
   using T = DTmaShape<ND, B, VPL>;
@@ -488,8 +497,10 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, 4)
   long long sent = 0;
   for (uint32_t tile = first; tile < (uint32_t)g.ntiles; tile += nwarps) {
     const TileXY tc = decode_tile(g, tile);
-    if (!tile_interior<ND, B, VPL>(g, tc)) continue;  // dq_decompress_edge_kernel
-    dfast_tile<ND, B, VPL, false>(fa, tile, tc, lane, ring, bars, prod, cons, nwarps, sent);
+    if (tile_interior<ND, B, VPL>(g, tc))
+      dfast_tile<ND, B, VPL, false>(fa, tile, tc, lane, ring, bars, prod, cons, nwarps, sent);
+    else if constexpr (EDGES)
+      dfast_tile<ND, B, VPL, true>(fa, tile, tc, lane, ring, bars, prod, cons, nwarps, sent);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) sent += __shfl_xor_sync(FULL, sent, o);
@@ -503,45 +514,6 @@ __host__ __device__ inline int64_t edge_tile_count(const Geo& g) {
   using S = Shape<ND, B, VPL>;
   const bool xp = (g.D2 % S::W) != 0, yp = (g.D1 % S::BY) != 0;
   return (xp ? g.P0 * g.P1 : 0) + (yp ? g.P0 * (g.NW - (xp ? 1 : 0)) : 0);
-}
-
-template <int ND, int B, int VPL>
-__global__ void __launch_bounds__(FAST_WARPS * 32, 4)
-    dq_decompress_edge_kernel(const __grid_constant__ DFastArgs fa) {
-  using S = Shape<ND, B, VPL>;
-  using F = DFastShape<ND, B, VPL>;
-  extern __shared__ __align__(128) unsigned char smem_dfast[];
-  const int lane = threadIdx.x & 31;
-  const int wib = threadIdx.x >> 5;
-  unsigned char* ring = smem_dfast + (size_t)wib * F::WARP_SMEM;
-  const Geo& g = fa.d.g;
-  const bool xp = (g.D2 % S::W) != 0;
-  const int64_t na = xp ? g.P0 * g.P1 : 0;
-  const int64_t nxb = g.NW - (xp ? 1 : 0);
-  const int64_t n = edge_tile_count<ND, B, VPL>(g);
-  const int64_t nwarps = (int64_t)gridDim.x * FAST_WARPS;
-  DProducer<ND, B, VPL> prod{};
-  Consumer<ND, B, VPL> cons{0, 0u};
-  long long sent = 0;
-  for (int64_t i = (int64_t)blockIdx.x * FAST_WARPS + wib; i < n; i += nwarps) {
-    TileXY tc;
-    if (i < na) {
-      tc.bz = (uint32_t)(i / g.P1);
-      tc.by = (uint32_t)(i % g.P1);
-      tc.wx = (uint32_t)(g.NW - 1);
-    } else {
-      const int64_t j = i - na;
-      tc.bz = (uint32_t)(j / nxb);
-      tc.by = (uint32_t)(g.P1 - 1);
-      tc.wx = (uint32_t)(j % nxb);
-    }
-    const uint32_t tile = (uint32_t)(((int64_t)tc.bz * g.P1 + tc.by) * g.NW + tc.wx);
-    dfast_tile<ND, B, VPL, true>(fa, tile, tc, lane, ring, nullptr, prod, cons, (uint32_t)nwarps,
-                                 sent);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) sent += __shfl_xor_sync(FULL, sent, o);
-  if (lane == 0 && sent) atomicAdd(fa.d.sentinels, (unsigned long long)sent);
 }
 
 }  // namespace vlz

@@ -1,7 +1,6 @@
 // k_decompress.cu -- reconstruction kernel instantiations and dispatch.
 //   fast shapes (3-D b=8/16, 2-D b=8/16), uint16 codes, aligned buffers:
 //       dq_decompress_fast_kernel (interior tiles, int32 with exactness check)
-//       + dq_decompress_edge_kernel (edge tiles, same recurrence)
 //       + dq_decompress_kernel<LIST> (flagged tiles, int64)
 //   everything else: dq_decompress_kernel (int64)
 #include "dq_decompress_fast.cuh"
@@ -43,13 +42,16 @@ static cudaError_t run_d(bool u32, const DecompressArgs& a, cudaStream_t st) {
       fa.d = a;
       fa.redo_count = const_cast<unsigned int*>(a.redo_count);
       fa.redo_list = const_cast<long long*>(a.redo_list);
-      auto kern = dq_decompress_fast_kernel<ND, B, VPL>;
+      const bool edges = edge_tile_count<ND, B, VPL>(a.g) > 0;
+      auto kern = edges ? dq_decompress_fast_kernel<ND, B, VPL, true>
+                        : dq_decompress_fast_kernel<ND, B, VPL, false>;
       int fsmem = dfast_smem_bytes<ND, B, VPL>();
       if constexpr (ND == 3 && B == 8 && VPL == 4) {
         // every block full (block b starts at b * 512): TMA tensor loads
         if (a.g.D0 % 8 == 0 && a.g.D1 % 8 == 0 && a.g.D2 % 8 == 0 &&
             a.g.nblocks < (1ll << 31) && make_code_map(&fa.tmap, a.codes, a.g.nblocks)) {
-          kern = dq_decompress_tma_kernel<ND, B, VPL>;
+          kern = edges ? dq_decompress_tma_kernel<ND, B, VPL, true>
+                       : dq_decompress_tma_kernel<ND, B, VPL, false>;
           fsmem = dtma_smem_bytes<ND, B, VPL>();
         }
       }
@@ -70,20 +72,6 @@ static cudaError_t run_d(bool u32, const DecompressArgs& a, cudaStream_t st) {
       g_launches.fetch_add(1, std::memory_order_relaxed);
       e = cudaGetLastError();
       if (e != cudaSuccess) return e;
-      const int64_t nedge = edge_tile_count<ND, B, VPL>(a.g);
-      if (nedge > 0) {
-        auto ekern = dq_decompress_edge_kernel<ND, B, VPL>;
-        e = cudaFuncSetAttribute(ekern, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem);
-        if (e != cudaSuccess) return e;
-        int64_t eg = (nedge + FAST_WARPS - 1) / FAST_WARPS;
-        if (eg > (int64_t)per_sm * num_sms()) eg = (int64_t)per_sm * num_sms();
-        if (t) timing_mark(TK_EDGE, true, st);
-        ekern<<<(unsigned)eg, FAST_WARPS * 32, fsmem, st>>>(fa);
-        if (t) timing_mark(TK_EDGE, false, st);
-        g_launches.fetch_add(1, std::memory_order_relaxed);
-        e = cudaGetLastError();
-        if (e != cudaSuccess) return e;
-      }
       auto redo = dq_decompress_kernel<ND, B, VPL, uint16_t, true>;
       if (smem > 48 * 1024) {
         e = cudaFuncSetAttribute(redo, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
