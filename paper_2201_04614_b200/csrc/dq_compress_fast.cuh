@@ -170,12 +170,12 @@ struct Producer {
   }
 };
 
-template <int ND, int B, int VPL>
+template <int ND, int B, int VPL, int NST = FAST_STAGES>
 struct Consumer {
   int stage;
   uint32_t parity;
   __device__ __forceinline__ void advance() {
-    if (++stage == FAST_STAGES) {
+    if (++stage == NST) {
       stage = 0;
       parity ^= 1u;
     }

@@ -6,7 +6,7 @@
 // for the throughput shapes (3-D b=8/16, 2-D b=8/16) and interior tiles:
 //
 //  * each lane streams its own VPL codes of every row of a plane into a
-//    per-warp shared ring with cp.async (LDGSTS), FAST_STAGES planes ahead
+//    per-warp shared ring with cp.async (LDGSTS), DSTAGES planes ahead
 //    and across tile boundaries; the [row][lane] layout makes the later
 //    vector LDS conflict-free and needs no cross-lane barrier;
 //  * arithmetic is wrapping int32.  It is exact whenever |s0| < 2^27 and every
@@ -34,6 +34,9 @@
 
 namespace vlz {
 
+// ring depth of the decompress producers (planes in flight per warp)
+constexpr int DSTAGES = 2;
+
 template <int ND, int B, int VPL>
 struct DFastShape {
   using S = Shape<ND, B, VPL>;
@@ -46,7 +49,7 @@ struct DFastShape {
   static constexpr int PREV_BYTES = (ND == 3) ? S::BY * S::W * 4 : 0;
   // edge tiles fill their codes synchronously into a slot of their own, so
   // the ring of interior planes keeps streaming underneath
-  static constexpr int EDGE_OFF = FAST_STAGES * STAGE_BYTES + PREV_BYTES;
+  static constexpr int EDGE_OFF = DSTAGES * STAGE_BYTES + PREV_BYTES;
   static constexpr int WARP_SMEM = EDGE_OFF + STAGE_BYTES;
 };
 
@@ -70,7 +73,7 @@ __device__ __forceinline__ bool tile_interior(const Geo& g, const TileXY& c) {
 
 // per-lane producer of code planes (interior tiles only; others are skipped).
 // Every issue() commits exactly one cp.async group (possibly empty), so
-// cp.async.wait_group<FAST_STAGES-1> always retires the plane being consumed.
+// cp.async.wait_group<DSTAGES-1> always retires the plane being consumed.
 template <int ND, int B, int VPL>
 struct DProducer {
   using S = Shape<ND, B, VPL>;
@@ -119,7 +122,7 @@ struct DProducer {
       }
     }
     cp_async_commit();
-    if (++stage == FAST_STAGES) stage = 0;
+    if (++stage == DSTAGES) stage = 0;
   }
 };
 
@@ -163,7 +166,7 @@ struct DTProducer {
       mbar_arrive_expect_tx(bar, (uint32_t)F::STAGE_BYTES);
       tma_load_3d(ring + stage * F::STAGE_BYTES, tmap, 0, zl, b0, bar);
     }
-    if (++stage == FAST_STAGES) stage = 0;
+    if (++stage == DSTAGES) stage = 0;
     if (++zl >= ez) {
       tile += nwarps;
       seek(g, nwarps);
@@ -174,7 +177,7 @@ struct DTProducer {
 template <int ND, int B, int VPL, bool EDGE, class Prod>
 __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, const TileXY& tc,
                                            int lane, unsigned char* ring, uint64_t* bars,
-                                           Prod& prod, Consumer<ND, B, VPL>& cons,
+                                           Prod& prod, Consumer<ND, B, VPL, DSTAGES>& cons,
                                            uint32_t nwarps, long long& sent_acc) {
   constexpr bool TMAP = Prod::TMAP;
   using S = Shape<ND, B, VPL>;
@@ -217,7 +220,7 @@ __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, c
   // state starts at s0; 1-D/2-D: the previous-row state does), so d = E + s0
   // comes out of the recurrence directly and a sentinel resets the x-scan to
   // d_s - E'(prev plane) - G(prev row) with no s0 term.
-  int* const pplane = reinterpret_cast<int*>(ring + FAST_STAGES * F::STAGE_BYTES) + lane * VPL;
+  int* const pplane = reinterpret_cast<int*>(ring + DSTAGES * F::STAGE_BYTES) + lane * VPL;
   if (ND == 3) {
 #pragma unroll 1
     for (int yl = 0; yl < BY; ++yl) {
@@ -257,7 +260,7 @@ __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, c
       mbar_wait(&bars[cons.stage], cons.parity);
     } else {
       slot = slot0 + cons.stage * F::STAGE_BYTES;
-      cp_async_wait<FAST_STAGES - 1>();
+      cp_async_wait<DSTAGES - 1>();
     }
     int grow[VPL];
 #pragma unroll
@@ -441,8 +444,8 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, 4)
   const uint32_t first = blockIdx.x * FAST_WARPS + wib;
   DProducer<ND, B, VPL> prod;
   prod.start(g, codes, first, nwarps, lane);
-  for (int s = 0; s < FAST_STAGES; ++s) prod.issue(g, codes, ring, nwarps, lane);
-  Consumer<ND, B, VPL> cons{0, 0u};
+  for (int s = 0; s < DSTAGES; ++s) prod.issue(g, codes, ring, nwarps, lane);
+  Consumer<ND, B, VPL, DSTAGES> cons{0, 0u};
   long long sent = 0;
   for (uint32_t tile = first; tile < (uint32_t)g.ntiles; tile += nwarps) {
     const TileXY tc = decode_tile(g, tile);
@@ -482,7 +485,7 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, 4)
   uint64_t* bars = reinterpret_cast<uint64_t*>(ring + T::BAR_OFF);
   const Geo& g = fa.d.g;
   if (lane == 0) {
-    for (int s = 0; s < FAST_STAGES; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < DSTAGES; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
   }
   __syncwarp();
@@ -492,8 +495,8 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, 4)
   const uint32_t first = blockIdx.x * FAST_WARPS + wib;
   DTProducer<ND, B, VPL> prod;
   prod.start(g, first, nwarps);
-  for (int s = 0; s < FAST_STAGES; ++s) prod.issue(g, &fa.tmap, ring, bars, lane, nwarps);
-  Consumer<ND, B, VPL> cons{0, 0u};
+  for (int s = 0; s < DSTAGES; ++s) prod.issue(g, &fa.tmap, ring, bars, lane, nwarps);
+  Consumer<ND, B, VPL, DSTAGES> cons{0, 0u};
   long long sent = 0;
   for (uint32_t tile = first; tile < (uint32_t)g.ntiles; tile += nwarps) {
     const TileXY tc = decode_tile(g, tile);
