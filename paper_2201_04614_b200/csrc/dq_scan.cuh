@@ -95,6 +95,7 @@ template <int SCAN_IPT>
 __global__ void __launch_bounds__(SCAN_THREADS) dq_scan_kernel(ScanArgs a) {
   constexpr int SCAN_CH = SCAN_THREADS * SCAN_IPT;
   __shared__ long long s_src[SCAN_CH];   // scratch source of each block's outliers
+  __shared__ long long s_cnt[SCAN_CH];   // counts in, final counts / offsets out
   __shared__ long long s_warp[SCAN_THREADS / 32];
   __shared__ long long s_excl;
   __shared__ unsigned int s_tile;
@@ -112,23 +113,33 @@ __global__ void __launch_bounds__(SCAN_THREADS) dq_scan_kernel(ScanArgs a) {
     s0 = stat_value(a.q.kind, gs[0], gs[1], gs[2], -gs[3]);
   }
 
-  long long c[SCAN_IPT];
-  long long tsum = 0;
+  // the chunk's count words move through shared memory so that global loads
+  // and stores are coalesced; thread t then owns blocks t*IPT .. t*IPT+IPT-1
+#pragma unroll
+  for (int k = 0; k < SCAN_IPT; ++k) {
+    const int64_t bi = base + (int64_t)k * SCAN_THREADS + tid;
+    s_cnt[k * SCAN_THREADS + tid] = bi < nb ? a.counts[bi] : 0;
+  }
+  __syncthreads();
+  // per-block counts fit 32 bits (<= block volume), so do chunk-local sums
+  // (<= SCAN_CH * 2^18); 32-bit state keeps the register count low
+  int c[SCAN_IPT];
+  int tsum = 0;
 #pragma unroll
   for (int k = 0; k < SCAN_IPT; ++k) {
     const int64_t bi = base + (int64_t)tid * SCAN_IPT + k;
     c[k] = 0;
     if (bi < nb) {
-      c[k] = a.counts[bi];
+      const long long rec = s_cnt[tid * SCAN_IPT + k];
+      c[k] = (int)rec;
       if (a.fix_origin || (a.gather && c[k] > 0)) {
         int64_t bstart, origin;
         block_of(a.g, bi, a.BZ, a.BY, a.BX, bstart, origin);
         if (a.fix_origin) {
           // pending-origin record written by the fused kernel (pack_origin)
-          const int64_t rec = c[k];
           const int d = (int)(rec >> 32);
           const bool bad = (rec >> 24) & 1;
-          c[k] = rec & 0xffffff;
+          c[k] = (int)(rec & 0xffffff);
           const int64_t delta = (int64_t)d - s0;
           const int R = a.q.radius;
           const bool out = bad || delta > (int64_t)(R - 1) || delta < -(int64_t)(R - 1);
@@ -148,7 +159,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) dq_scan_kernel(ScanArgs a) {
             a.scratch[bstart] = a.in[origin];  // verbatim value, read only for outliers
             c[k] += 1;
           }
-          a.counts[bi] = c[k];
+          s_cnt[tid * SCAN_IPT + k] = c[k];  // final count, stored coalesced below
           s_src[tid * SCAN_IPT + k] = bstart + (out ? 0 : 1);
         } else {
           s_src[tid * SCAN_IPT + k] = bstart + (a.codes[bstart] == 0 ? 0 : 1);
@@ -158,21 +169,21 @@ __global__ void __launch_bounds__(SCAN_THREADS) dq_scan_kernel(ScanArgs a) {
     tsum += c[k];
   }
   // block-wide exclusive scan of the per-thread sums
-  long long inc = tsum;
+  int inc = tsum;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    const long long u = __shfl_up_sync(FULL, inc, o);
+    const int u = __shfl_up_sync(FULL, inc, o);
     if (lane >= o) inc += u;
   }
   if (lane == 31) s_warp[wid] = inc;
   __syncthreads();
-  long long wbase = 0, agg = 0;
+  int wbase = 0, agg = 0;
 #pragma unroll
   for (int w = 0; w < SCAN_THREADS / 32; ++w) {
-    if (w < wid) wbase += s_warp[w];
-    agg += s_warp[w];
+    if (w < wid) wbase += (int)s_warp[w];
+    agg += (int)s_warp[w];
   }
-  const long long texcl = wbase + inc - tsum;
+  const int texcl = wbase + inc - tsum;
 
   // decoupled look-back (warp 0)
   if (wid == 0) {
@@ -225,23 +236,31 @@ __global__ void __launch_bounds__(SCAN_THREADS) dq_scan_kernel(ScanArgs a) {
   // copies the outliers of its own blocks -- all copies of the chunk are in
   // flight at once -- and blocks with >= 32 outliers are copied by the whole
   // warp, coalesced
-  long long run = texcl;
+  int run = texcl;  // chunk-local offset
   unsigned heavy = 0;
-  long long hdst[SCAN_IPT];
+  int hdst[SCAN_IPT];
+  float* const outc = a.out + cexcl;
 #pragma unroll
   for (int k = 0; k < SCAN_IPT; ++k) {
-    const int64_t bi = base + (int64_t)tid * SCAN_IPT + k;
-    const long long dst = cexcl + run;
-    hdst[k] = dst;
+    hdst[k] = run;
     if (!a.gather) {
-      if (bi < nb) a.offsets[bi] = dst;
+      s_cnt[tid * SCAN_IPT + k] = cexcl + run;  // offset, stored coalesced below
     } else if (c[k] > 0 && c[k] < 32) {
       const float* src = a.scratch + s_src[tid * SCAN_IPT + k];
-      for (long long t = 0; t < c[k]; ++t) a.out[dst + t] = src[t];
+      for (int t = 0; t < c[k]; ++t) outc[run + t] = src[t];
     } else if (c[k] >= 32) {
       heavy |= 1u << k;
     }
     run += c[k];
+  }
+  if (!a.gather || a.fix_origin) {  // offsets, or the fixed counts, go out coalesced
+    __syncthreads();
+    int64_t* dst = a.gather ? a.counts : a.offsets;
+#pragma unroll
+    for (int k = 0; k < SCAN_IPT; ++k) {
+      const int64_t bi = base + (int64_t)k * SCAN_THREADS + tid;
+      if (bi < nb) dst[bi] = s_cnt[k * SCAN_THREADS + tid];
+    }
   }
   if (!a.gather) return;
   unsigned hm = __ballot_sync(FULL, heavy != 0);
@@ -252,20 +271,20 @@ __global__ void __launch_bounds__(SCAN_THREADS) dq_scan_kernel(ScanArgs a) {
 #pragma unroll
     for (int k = 0; k < SCAN_IPT; ++k) {
       if (!((mk >> k) & 1u)) continue;  // warp-uniform
-      const long long n = __shfl_sync(FULL, c[k], src_lane);
-      const long long dst = __shfl_sync(FULL, hdst[k], src_lane);
+      const int n = __shfl_sync(FULL, c[k], src_lane);
+      const int dst = __shfl_sync(FULL, hdst[k], src_lane);
       const float* src = a.scratch + s_src[(tid - lane + src_lane) * SCAN_IPT + k];
-      for (long long t0 = 0; t0 < n; t0 += 128) {
+      for (int t0 = 0; t0 < n; t0 += 128) {
         float v[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const long long t = t0 + lane + 32 * j;
+          const int t = t0 + lane + 32 * j;
           if (t < n) v[j] = __ldg(src + t);
         }
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const long long t = t0 + lane + 32 * j;
-          if (t < n) a.out[dst + t] = v[j];
+          const int t = t0 + lane + 32 * j;
+          if (t < n) outc[dst + t] = v[j];
         }
       }
     }
