@@ -430,7 +430,7 @@ __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, c
 // registers of a second instantiation of the tile body); grids without them
 // take the lean variant
 template <int ND, int B, int VPL, bool EDGES>
-__global__ void __launch_bounds__(FAST_WARPS * 32, 4)
+__global__ void __launch_bounds__(FAST_WARPS * 32, (EDGES && B == 8) ? 3 : 4)
     dq_decompress_fast_kernel(const __grid_constant__ DFastArgs fa) {
   using F = DFastShape<ND, B, VPL>;
   extern __shared__ __align__(128) unsigned char smem_dfast[];
@@ -473,7 +473,7 @@ __host__ __device__ constexpr int dtma_smem_bytes() {
 }
 
 template <int ND, int B, int VPL, bool EDGES>
-__global__ void __launch_bounds__(FAST_WARPS * 32, 4)
+__global__ void __launch_bounds__(FAST_WARPS * 32, (EDGES && B == 8) ? 3 : 4)
     dq_decompress_tma_kernel(const __grid_constant__ DFastArgs fa) {
   using T = DTmaShape<ND, B, VPL>;
   extern __shared__ __align__(1024) unsigned char smem_dtma[];
