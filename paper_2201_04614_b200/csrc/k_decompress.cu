@@ -100,7 +100,7 @@ cudaError_t launch_decompress(int nd, int B, bool u32, const DecompressArgs& a, 
   } else if (nd == 2) {
     switch (B) {
       case 8: return run_d<2, 8, 4>(u32, a, st);
-      case 16: return run_d<2, 16, 2>(u32, a, st);
+      case 16: return run_d<2, 16, 4>(u32, a, st);
       case 32: return run_d<2, 32, 4>(u32, a, st);
       case 64: return run_d<2, 64, 4>(u32, a, st);
     }

@@ -14,6 +14,7 @@ import os
 import statistics
 import sys
 
+import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -126,6 +127,24 @@ def main():
         c4 = workloads.gen_c4(512)
         run("C4 b=8 R=512", c4, 1e-3, 8, "mean:global", 512)
         run("C4 b=16 R=32768", c4, 1e-3, 16, "mean:global", 32768)
+    if "1D" in which:  # large 1-D stream (C1 recipe at 256 M elements)
+        rng = np.random.default_rng(5)
+        n = 256 * 1024 * 1024
+        walk = np.cumsum(rng.normal(0, 1, n).astype(np.float32)) * np.float32(0.01)
+        big = (walk + np.sin(np.arange(n, dtype=np.float32) * np.float32(2 * np.pi / 4096)))
+        big = big.astype(np.float32)
+        run("1D 256M b=256", big, 1e-4, 256, "zero", 512)
+        run("1D 256M b=64 mean:global", big, 1e-4, 64, "mean:global", 512)
+    if "2D" in which:  # large 2-D field (C2 recipe at 16384 x 16384)
+        rng = np.random.default_rng(6)
+        y, x = np.meshgrid(np.linspace(0, 1, 16384, dtype=np.float32),
+                           np.linspace(0, 1, 16384, dtype=np.float32), indexing="ij")
+        f = np.zeros((16384, 16384), np.float32)
+        for _ in range(8):
+            ky, kx = rng.integers(1, 16, 2)
+            f += np.sin(2 * np.pi * (ky * y + kx * x) + rng.uniform(0, 6.28)).astype(np.float32)
+        run("2D 16384^2 b=16 mean:block", f, 1e-4, 16, "mean:block", 512)
+        run("2D 16384^2 b=8 zero", f, 1e-4, 8, "zero", 512)
     if "stress" in which:
         c4 = workloads.gen_c4(256)
         run("stress b=8 R=512 eb=1e-5", c4, 1e-5, 8, "mean:global", 512)
