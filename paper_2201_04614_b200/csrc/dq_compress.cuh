@@ -43,6 +43,7 @@ struct CompressArgs {
   float* scratch;  // N floats, block-relative outlier slots
   int64_t* counts;
   int64_t* scalars;
+  float* origin_vals;  // *:global: verbatim origin value per block (workspace, coalesced)
   unsigned long long* first_nonfinite;  // device result fields (atomicMin)
   unsigned long long* first_overflow;
   unsigned long long* gsum;  // global statistics accumulators
@@ -339,6 +340,7 @@ __device__ __forceinline__ bool compress_tile(const CompressArgs& a, int64_t til
     // *:global: the origin is still pending -- hand the scan kernel its
     // prequantized value and narrowing verdict packed beside the count
     a.counts[bi] = (MODE == MODE_GLOBAL) ? pack_origin(total, d_origin, bad_origin) : total;
+    if (MODE == MODE_GLOBAL) a.origin_vals[bi] = v_origin;
   }
   return false;
 }

@@ -520,6 +520,7 @@ __device__ __forceinline__ void fast_tile(const FastArgs& fa, uint32_t tile, con
     // *:global: the origin is still pending -- hand the scan kernel its
     // prequantized value and narrowing verdict packed beside the count
     a.counts[bi] = (MODE == MODE_GLOBAL) ? pack_origin(total, d_origin, bad_origin) : total;
+    if (MODE == MODE_GLOBAL) a.origin_vals[bi] = v_origin;
   }
 }
 

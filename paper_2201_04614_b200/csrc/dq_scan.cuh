@@ -39,6 +39,7 @@ inline int64_t scan_chunks(int64_t nblocks) {
   return n < 1 ? 1 : n;
 }
 
+
 struct ScanArgs {
   Geo g;
   QP q;
@@ -46,6 +47,7 @@ struct ScanArgs {
   int fix_origin;  // 1: resolve pending origins (*:global policies)
   int gather;      // 1: compact outliers; 0: write offsets
   const float* in;
+  const float* origin_vals;  // *:global: verbatim origin value per block (fused kernel)
   uint16_t* codes;
   int64_t* counts;
   float* scratch;
@@ -91,178 +93,277 @@ constexpr unsigned long long FLAG_A = 1ull << 62;
 constexpr unsigned long long FLAG_P = 2ull << 62;
 constexpr unsigned long long VAL_MASK = (1ull << 62) - 1;
 
+// shared-memory padding: element i of a chunk staged as [k][tid] (coalesced
+// global side) and read as [tid][k] (IPT consecutive blocks per thread).
+// 8-byte words: one pad word per IPT words (thread rows land on distinct
+// bank pairs); 4-byte words: one per 32.
+template <int IPT>
+__device__ __forceinline__ int pad_l(int i) { return i + i / IPT; }
+__device__ __forceinline__ int pad_f(int i) { return i + (i >> 5); }
+
+// publish a chunk's aggregate (thread 0) as soon as it is known
+__device__ __forceinline__ void publish_aggregate(unsigned long long* lb, int64_t tile,
+                                                  long long agg) {
+  if (threadIdx.x == 0) {
+    cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> me(lb[tile]);
+    me.store((tile == 0 ? FLAG_P : FLAG_A) | (unsigned long long)agg, cuda::memory_order_relaxed);
+  }
+}
+
+// Decoupled look-back with the whole CTA: every round, thread t inspects
+// predecessor tile-1-t (SCAN_THREADS flags per L2 round trip instead of 32;
+// the other warps would only wait at the barrier otherwise).  Returns the
+// chunk's exclusive prefix in every thread and publishes the inclusive one.
+__device__ __forceinline__ long long lookback_cta(unsigned long long* lb, int64_t tile,
+                                                  long long agg, int* s_first,
+                                                  long long* s_wsum) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  constexpr int NW = SCAN_THREADS / 32;
+  long long excl = 0;
+  int64_t pred = tile - 1;
+  while (pred >= 0) {  // uniform across the CTA
+    const int64_t idx = pred - tid;
+    unsigned long long w = FLAG_P;  // before chunk 0: an inclusive prefix of 0
+    if (idx >= 0) {
+      cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> r(lb[idx]);
+      w = r.load(cuda::memory_order_relaxed);
+      while ((w >> 62) == 0) w = r.load(cuda::memory_order_relaxed);
+    }
+    const unsigned pm = __ballot_sync(FULL, (w >> 62) == 2);
+    if (lane == 0) s_first[wid] = pm ? wid * 32 + __ffs(pm) - 1 : SCAN_THREADS;
+    __syncthreads();
+    int stop = SCAN_THREADS;
+#pragma unroll
+    for (int k = 0; k < NW; ++k) stop = min(stop, s_first[k]);
+    long long val = (tid <= stop) ? (long long)(w & VAL_MASK) : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(FULL, val, o);
+    if (lane == 0) s_wsum[wid] = val;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < NW; ++k) excl += s_wsum[k];
+    __syncthreads();  // s_first / s_wsum are rewritten by the next round
+    if (stop < SCAN_THREADS) break;
+    pred -= SCAN_THREADS;
+  }
+  if (tid == 0 && tile > 0) {
+    cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> me(lb[tile]);
+    me.store(FLAG_P | (unsigned long long)(excl + agg), cuda::memory_order_relaxed);
+  }
+  return excl;
+}
+
+// block-wide exclusive scan of one value per thread; also returns the total
+template <typename T>
+__device__ __forceinline__ T cta_excl_scan(T v, T* s_warp, T& total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  T inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const T u = __shfl_up_sync(FULL, inc, o);
+    if (lane >= o) inc += u;
+  }
+  if (lane == 31) s_warp[wid] = inc;
+  __syncthreads();
+  T wbase = 0, agg = 0;
+#pragma unroll
+  for (int w = 0; w < SCAN_THREADS / 32; ++w) {
+    if (w < wid) wbase += s_warp[w];
+    agg += s_warp[w];
+  }
+  total = agg;
+  return wbase + inc - v;
+}
+
+// Compress: origin fix-up (*:global), count scan and outlier gather.  Thread t
+// owns blocks t*IPT .. t*IPT+IPT-1 of its chunk.  Order of work:
+//  1. counts from the records (shared memory) -> chunk scan -> the aggregate
+//     is published at once (successors' look-backs need nothing else);
+//  2. the scattered work that does not depend on the chunk's offset -- origin
+//     code rewrites, slot-0 probes, the first scratch outlier of every block --
+//     is issued, so its latency overlaps the look-back;
+//  3. CTA-wide look-back, then the compact stores.
+// Under *:global the origin's verbatim value comes from the fused kernel's
+// per-block side array (read coalesced) and goes straight into the compact
+// array; the other outliers come from the block's scratch slots 1.. (0.. when
+// a non-global origin sits in slot 0).
 template <int SCAN_IPT>
 __global__ void __launch_bounds__(SCAN_THREADS) dq_scan_kernel(ScanArgs a) {
   constexpr int SCAN_CH = SCAN_THREADS * SCAN_IPT;
-  __shared__ long long s_src[SCAN_CH];   // scratch source of each block's outliers
-  __shared__ long long s_cnt[SCAN_CH];   // counts in, final counts / offsets out
-  __shared__ long long s_warp[SCAN_THREADS / 32];
-  __shared__ long long s_excl;
+  constexpr int HEAVY = 32;  // blocks with >= HEAVY scratch outliers: whole-warp copy
+  // padded so that both the coalesced ([k][tid]) and the per-thread
+  // ([tid][k]) access patterns are (nearly) bank-conflict free
+  __shared__ long long s_rec[SCAN_CH + SCAN_THREADS];  // count records in, final counts out
+  __shared__ float s_vo[SCAN_CH + SCAN_CH / 32];       // *:global: origin values
+  __shared__ int s_warp[SCAN_THREADS / 32];
+  __shared__ int s_first[SCAN_THREADS / 32];
+  __shared__ long long s_wsum[SCAN_THREADS / 32];
   __shared__ unsigned int s_tile;
 
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31;
   if (tid == 0) s_tile = atomicAdd(a.ticket, 1u);
   __syncthreads();
   const int64_t tile = s_tile;
   const int64_t base = tile * SCAN_CH;
   const int64_t nb = a.g.nblocks;
+  const float* __restrict__ scratch = a.scratch;
+  const bool fix = a.fix_origin != 0;
 
   int64_t s0 = 0;
-  if (a.fix_origin) {
+  if (fix) {
     const long long* gs = a.gstats;
     s0 = stat_value(a.q.kind, gs[0], gs[1], gs[2], -gs[3]);
   }
 
-  // the chunk's count words move through shared memory so that global loads
-  // and stores are coalesced; thread t then owns blocks t*IPT .. t*IPT+IPT-1
 #pragma unroll
   for (int k = 0; k < SCAN_IPT; ++k) {
     const int64_t bi = base + (int64_t)k * SCAN_THREADS + tid;
-    s_cnt[k * SCAN_THREADS + tid] = bi < nb ? a.counts[bi] : 0;
+    s_rec[pad_l<SCAN_IPT>(k * SCAN_THREADS + tid)] = bi < nb ? a.counts[bi] : 0;
+    if (fix) s_vo[pad_f(k * SCAN_THREADS + tid)] = bi < nb ? a.origin_vals[bi] : 0.f;
   }
   __syncthreads();
-  // per-block counts fit 32 bits (<= block volume), so do chunk-local sums
-  // (<= SCAN_CH * 2^18); 32-bit state keeps the register count low
+
+  // 1. counts (and, under *:global, the origin verdicts) from the records
   int c[SCAN_IPT];
+  unsigned omask = 0;  // *:global: origin is an outlier
+  unsigned wmask = 0;  // *:global: origin code must be rewritten
+  uint16_t ocode[SCAN_IPT];
+  float vo[SCAN_IPT];
   int tsum = 0;
+  const int R = a.q.radius;
 #pragma unroll
   for (int k = 0; k < SCAN_IPT; ++k) {
     const int64_t bi = base + (int64_t)tid * SCAN_IPT + k;
+    const long long rec = s_rec[pad_l<SCAN_IPT>(tid * SCAN_IPT + k)];
     c[k] = 0;
+    ocode[k] = 0;
+    vo[k] = 0.f;
     if (bi < nb) {
-      const long long rec = s_cnt[tid * SCAN_IPT + k];
-      c[k] = (int)rec;
-      if (a.fix_origin || (a.gather && c[k] > 0)) {
-        int64_t bstart, origin;
-        block_of(a.g, bi, a.BZ, a.BY, a.BX, bstart, origin);
-        if (a.fix_origin) {
-          // pending-origin record written by the fused kernel (pack_origin)
-          const int d = (int)(rec >> 32);
-          const bool bad = (rec >> 24) & 1;
-          c[k] = (int)(rec & 0xffffff);
-          const int64_t delta = (int64_t)d - s0;
-          const int R = a.q.radius;
-          const bool out = bad || delta > (int64_t)(R - 1) || delta < -(int64_t)(R - 1);
-          const uint16_t code = out ? (uint16_t)0 : (uint16_t)(delta + R);
-          // the fused kernel already stored the s0 = 0 code of the origin;
-          // rewrite only when s0 changes it (saves a sector read-modify-write
-          // per block when the global scalar is 0)
-          const bool out0 = bad || d > R - 1 || d < -(R - 1);
-          const uint16_t code0 = out0 ? (uint16_t)0 : (uint16_t)(d + R);
-          if (code != code0) {
-            a.codes[bstart] = code;
-            if (a.patch_list)
-              a.patch_list[atomicAdd(a.patch_count, 1u)] =
-                  ((unsigned long long)bstart << 16) | (unsigned long long)code;
-          }
-          if (out) {
-            a.scratch[bstart] = a.in[origin];  // verbatim value, read only for outliers
-            c[k] += 1;
-          }
-          s_cnt[tid * SCAN_IPT + k] = c[k];  // final count, stored coalesced below
-          s_src[tid * SCAN_IPT + k] = bstart + (out ? 0 : 1);
-        } else {
-          s_src[tid * SCAN_IPT + k] = bstart + (a.codes[bstart] == 0 ? 0 : 1);
+      if (fix) {
+        // pending-origin record written by the fused kernel (pack_origin)
+        const int d = (int)(rec >> 32);
+        const bool bad = (rec >> 24) & 1;
+        const int64_t delta = (int64_t)d - s0;
+        const bool out = bad || delta > (int64_t)(R - 1) || delta < -(int64_t)(R - 1);
+        ocode[k] = out ? (uint16_t)0 : (uint16_t)(delta + R);
+        // the fused kernel already stored the s0 = 0 code of the origin;
+        // rewrite only when s0 changes it
+        const bool out0 = bad || d > R - 1 || d < -(R - 1);
+        const uint16_t c0 = out0 ? (uint16_t)0 : (uint16_t)(d + R);
+        if (ocode[k] != c0) wmask |= 1u << k;
+        if (out) {
+          omask |= 1u << k;
+          vo[k] = s_vo[pad_f(tid * SCAN_IPT + k)];
         }
+        c[k] = (int)(rec & 0xffffff) + (out ? 1 : 0);
+        s_rec[pad_l<SCAN_IPT>(tid * SCAN_IPT + k)] = c[k];  // final count (ordered by the scan's barrier)
+      } else {
+        c[k] = (int)rec;
       }
     }
     tsum += c[k];
   }
-  // block-wide exclusive scan of the per-thread sums
-  int inc = tsum;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int u = __shfl_up_sync(FULL, inc, o);
-    if (lane >= o) inc += u;
-  }
-  if (lane == 31) s_warp[wid] = inc;
-  __syncthreads();
-  int wbase = 0, agg = 0;
-#pragma unroll
-  for (int w = 0; w < SCAN_THREADS / 32; ++w) {
-    if (w < wid) wbase += (int)s_warp[w];
-    agg += (int)s_warp[w];
-  }
-  const int texcl = wbase + inc - tsum;
-
-  // decoupled look-back (warp 0)
-  if (wid == 0) {
-    cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> me(a.lb[tile]);
-    if (lane == 0) me.store((tile == 0 ? FLAG_P : FLAG_A) | (unsigned long long)agg,
-                            cuda::memory_order_relaxed);
-    long long excl = 0;
-    int64_t pred = tile - 1;
-    while (pred >= 0) {
-      const int64_t idx = pred - lane;
-      unsigned long long w = FLAG_P;
-      if (idx >= 0) {
-        cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> r(a.lb[idx]);
-        w = r.load(cuda::memory_order_relaxed);
-        while ((w >> 62) == 0) w = r.load(cuda::memory_order_relaxed);
-      }
-      const unsigned pm = __ballot_sync(FULL, (w >> 62) == 2);
-      const int stop = pm ? __ffs(pm) - 1 : 31;
-      long long val = (lane <= stop) ? (long long)(w & VAL_MASK) : 0;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(FULL, val, o);
-      excl += val;
-      if (pm) break;
-      pred -= 32;
-    }
-    if (lane == 0) {
-      if (tile > 0) me.store(FLAG_P | (unsigned long long)(excl + agg), cuda::memory_order_relaxed);
-      s_excl = excl;
-      if (base + SCAN_CH >= nb) {
-        *a.n_out = excl + agg;
-        if (a.fix_origin && a.scalars) a.scalars[0] = s0;
-        if (a.status) {
-          // quantize.py:62-72 precedence: any non-finite value first, then overflow
-          const unsigned long long nf = *a.first_nonfinite, ov = *a.first_overflow;
-          if (nf != 0x7fffffffffffffffull) {
-            *a.status = 1;  // VLZ_ST_NONFINITE
-            *a.index = (long long)nf;
-          } else if (ov != 0x7fffffffffffffffull) {
-            *a.status = 2;  // VLZ_ST_OVERFLOW
-            *a.index = (long long)ov;
-          }
-        }
-      }
-    }
-  }
-  __syncthreads();
-  const long long cexcl = s_excl;
-
-  // per-block offsets (decompress) or outlier gather (compress): each thread
-  // copies the outliers of its own blocks -- all copies of the chunk are in
-  // flight at once -- and blocks with >= 32 outliers are copied by the whole
-  // warp, coalesced
-  int run = texcl;  // chunk-local offset
-  unsigned heavy = 0;
-  int hdst[SCAN_IPT];
-  float* const outc = a.out + cexcl;
-#pragma unroll
-  for (int k = 0; k < SCAN_IPT; ++k) {
-    hdst[k] = run;
-    if (!a.gather) {
-      s_cnt[tid * SCAN_IPT + k] = cexcl + run;  // offset, stored coalesced below
-    } else if (c[k] > 0 && c[k] < 32) {
-      const float* src = a.scratch + s_src[tid * SCAN_IPT + k];
-      for (int t = 0; t < c[k]; ++t) outc[run + t] = src[t];
-    } else if (c[k] >= 32) {
-      heavy |= 1u << k;
-    }
-    run += c[k];
-  }
-  if (!a.gather || a.fix_origin) {  // offsets, or the fixed counts, go out coalesced
-    __syncthreads();
-    int64_t* dst = a.gather ? a.counts : a.offsets;
+  int agg;
+  const int texcl = cta_excl_scan<int>(tsum, s_warp, agg);
+  publish_aggregate(a.lb, tile, agg);
+  if (fix) {
 #pragma unroll
     for (int k = 0; k < SCAN_IPT; ++k) {
       const int64_t bi = base + (int64_t)k * SCAN_THREADS + tid;
-      if (bi < nb) dst[bi] = s_cnt[k * SCAN_THREADS + tid];
+      if (bi < nb) a.counts[bi] = s_rec[pad_l<SCAN_IPT>(k * SCAN_THREADS + tid)];
     }
   }
-  if (!a.gather) return;
+
+  // 2. scattered work that does not need the chunk offset
+  int64_t src[SCAN_IPT];  // first scratch slot of the block's remaining outliers
+  int rem[SCAN_IPT];      // outliers left after the (register) origin
+  float v0[SCAN_IPT];     // first of them, prefetched
+  unsigned heavy = 0;
+  int tmax = 0;
+  if (fix) {
+#pragma unroll
+    for (int k = 0; k < SCAN_IPT; ++k) {
+      const int64_t bi = base + (int64_t)tid * SCAN_IPT + k;
+      rem[k] = c[k] - (int)((omask >> k) & 1u);
+      src[k] = 0;
+      if (((wmask >> k) & 1u) || rem[k] > 0) {
+        int64_t bstart, origin;
+        block_of(a.g, bi, a.BZ, a.BY, a.BX, bstart, origin);
+        src[k] = bstart + 1;
+        if ((wmask >> k) & 1u) {
+          a.codes[bstart] = ocode[k];
+          if (a.patch_list)
+            a.patch_list[atomicAdd(a.patch_count, 1u)] =
+                ((unsigned long long)bstart << 16) | (unsigned long long)ocode[k];
+        }
+      }
+    }
+  } else {
+    uint16_t code0[SCAN_IPT];
+#pragma unroll
+    for (int k = 0; k < SCAN_IPT; ++k) {
+      const int64_t bi = base + (int64_t)tid * SCAN_IPT + k;
+      rem[k] = c[k];
+      src[k] = 0;
+      code0[k] = 1;
+      if (c[k] > 0) {
+        int64_t bstart, origin;
+        block_of(a.g, bi, a.BZ, a.BY, a.BX, bstart, origin);
+        src[k] = bstart;
+        code0[k] = a.codes[bstart];  // 0: the origin is an outlier in slot 0
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < SCAN_IPT; ++k) src[k] += code0[k] == 0 ? 0 : 1;
+  }
+#pragma unroll
+  for (int k = 0; k < SCAN_IPT; ++k) {
+    if (rem[k] >= HEAVY) {
+      heavy |= 1u << k;
+      rem[k] = 0;
+    }
+    tmax = max(tmax, rem[k]);
+    v0[k] = 0.f;
+    if (rem[k] > 0) v0[k] = __ldg(scratch + src[k]);
+  }
+
+  // 3. look-back, then the compact stores
+  const long long cexcl = lookback_cta(a.lb, tile, agg, s_first, s_wsum);
+  if (tid == 0 && base + SCAN_CH >= nb) {
+    *a.n_out = cexcl + agg;
+    if (fix && a.scalars) a.scalars[0] = s0;
+    if (a.status) {
+      // quantize.py:62-72 precedence: any non-finite value first, then overflow
+      const unsigned long long nf = *a.first_nonfinite, ov = *a.first_overflow;
+      if (nf != 0x7fffffffffffffffull) {
+        *a.status = 1;  // VLZ_ST_NONFINITE
+        *a.index = (long long)nf;
+      } else if (ov != 0x7fffffffffffffffull) {
+        *a.status = 2;  // VLZ_ST_OVERFLOW
+        *a.index = (long long)ov;
+      }
+    }
+  }
+  float* const outc = a.out + cexcl;
+  int dst[SCAN_IPT];
+  int run = texcl;
+#pragma unroll
+  for (int k = 0; k < SCAN_IPT; ++k) {
+    const int first = (omask >> k) & 1u;
+    if (first) outc[run] = vo[k];
+    dst[k] = run + first;
+    if (rem[k] > 0) outc[dst[k]] = v0[k];
+    run += c[k];
+  }
+  for (int t = 1; t < tmax; ++t) {
+    float v[SCAN_IPT];
+#pragma unroll
+    for (int k = 0; k < SCAN_IPT; ++k)
+      if (t < rem[k]) v[k] = __ldg(scratch + src[k] + t);
+#pragma unroll
+    for (int k = 0; k < SCAN_IPT; ++k)
+      if (t < rem[k]) outc[dst[k] + t] = v[k];
+  }
   unsigned hm = __ballot_sync(FULL, heavy != 0);
   while (hm) {
     const int src_lane = __ffs(hm) - 1;
@@ -271,23 +372,120 @@ __global__ void __launch_bounds__(SCAN_THREADS) dq_scan_kernel(ScanArgs a) {
 #pragma unroll
     for (int k = 0; k < SCAN_IPT; ++k) {
       if (!((mk >> k) & 1u)) continue;  // warp-uniform
-      const int n = __shfl_sync(FULL, c[k], src_lane);
-      const int dst = __shfl_sync(FULL, hdst[k], src_lane);
-      const float* src = a.scratch + s_src[(tid - lane + src_lane) * SCAN_IPT + k];
+      const int first = __shfl_sync(FULL, (int)((omask >> k) & 1u), src_lane);
+      const int n = __shfl_sync(FULL, c[k], src_lane) - first;
+      const int d0 = __shfl_sync(FULL, dst[k], src_lane);
+      const int64_t s = __shfl_sync(FULL, src[k], src_lane);
       for (int t0 = 0; t0 < n; t0 += 128) {
         float v[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const int t = t0 + lane + 32 * j;
-          if (t < n) v[j] = __ldg(src + t);
+          if (t < n) v[j] = __ldg(scratch + s + t);
         }
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const int t = t0 + lane + 32 * j;
-          if (t < n) outc[dst + t] = v[j];
+          if (t < n) outc[d0 + t] = v[j];
         }
       }
     }
+  }
+}
+
+// Decompress: exclusive per-block outlier offsets (counts are the stream's
+// int64 values, summed in int64).  Reduce-then-scan inside one kernel: the
+// CTA holding ticket t owns a contiguous range of OFF_SPAN blocks (tens of KB
+// of counts), sums it with 8 independent coalesced loads per thread in
+// flight, publishes the sum for the look-back (one look-back per range, so
+// the chain is short), then re-reads the range -- an L2 hit -- and writes the
+// offsets, 2048 blocks per sweep staged through shared memory.
+constexpr int OFF_IPT = 8;
+constexpr int OFF_SWEEP = SCAN_THREADS * OFF_IPT;
+inline int64_t offsets_span(int64_t nblocks) {
+  // ~4 ranges per SM, at least one sweep each
+  int64_t span = (nblocks + 148 * 4 - 1) / (148 * 4);
+  span = (span + OFF_SWEEP - 1) / OFF_SWEEP * OFF_SWEEP;
+  return span < OFF_SWEEP ? OFF_SWEEP : span;
+}
+inline int64_t offsets_chunks(int64_t nblocks) {
+  const int64_t span = offsets_span(nblocks);
+  const int64_t n = (nblocks + span - 1) / span;
+  return n < 1 ? 1 : n;
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS) dq_offsets_kernel(ScanArgs a, int64_t span) {
+  __shared__ long long s_val[OFF_SWEEP + SCAN_THREADS];  // padded (pad_l)
+  __shared__ long long s_warp[SCAN_THREADS / 32];
+  __shared__ int s_first[SCAN_THREADS / 32];
+  __shared__ long long s_wsum[SCAN_THREADS / 32];
+  __shared__ unsigned int s_tile;
+  const int tid = threadIdx.x;
+  if (tid == 0) s_tile = atomicAdd(a.ticket, 1u);
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const int64_t nb = a.g.nblocks;
+  const int64_t lo = tile * span;
+  const int64_t hi = lo + span < nb ? lo + span : nb;
+  const int64_t* __restrict__ counts = a.counts;
+
+  long long part = 0;
+#pragma unroll 2
+  for (int64_t b0 = lo; b0 < hi; b0 += OFF_SWEEP) {
+    long long v[OFF_IPT];
+#pragma unroll
+    for (int k = 0; k < OFF_IPT; ++k) {
+      const int64_t bi = b0 + (int64_t)k * SCAN_THREADS + tid;
+      v[k] = bi < hi ? counts[bi] : 0;
+    }
+#pragma unroll
+    for (int k = 0; k < OFF_IPT; ++k) part += v[k];
+  }
+  long long agg;
+  cta_excl_scan<long long>(part, s_warp, agg);
+  publish_aggregate(a.lb, tile, agg);
+  // first sweep of the second pass in flight during the look-back
+  long long nxt[OFF_IPT];
+#pragma unroll
+  for (int k = 0; k < OFF_IPT; ++k) {
+    const int64_t bi = lo + (int64_t)k * SCAN_THREADS + tid;
+    nxt[k] = bi < hi ? counts[bi] : 0;
+  }
+  long long carry = lookback_cta(a.lb, tile, agg, s_first, s_wsum);
+  if (tid == 0 && hi >= nb) *a.n_out = carry + agg;
+  for (int64_t b0 = lo; b0 < hi; b0 += OFF_SWEEP) {
+#pragma unroll
+    for (int k = 0; k < OFF_IPT; ++k) s_val[pad_l<OFF_IPT>(k * SCAN_THREADS + tid)] = nxt[k];
+    if (b0 + OFF_SWEEP < hi) {  // next sweep in flight during this one
+#pragma unroll
+      for (int k = 0; k < OFF_IPT; ++k) {
+        const int64_t bi = b0 + OFF_SWEEP + (int64_t)k * SCAN_THREADS + tid;
+        nxt[k] = bi < hi ? counts[bi] : 0;
+      }
+    }
+    __syncthreads();
+    long long v[OFF_IPT];
+    long long tsum = 0;
+#pragma unroll
+    for (int k = 0; k < OFF_IPT; ++k) {
+      v[k] = s_val[pad_l<OFF_IPT>(tid * OFF_IPT + k)];
+      tsum += v[k];
+    }
+    long long sweep;
+    long long run = carry + cta_excl_scan<long long>(tsum, s_warp, sweep);
+#pragma unroll
+    for (int k = 0; k < OFF_IPT; ++k) {
+      s_val[pad_l<OFF_IPT>(tid * OFF_IPT + k)] = run;
+      run += v[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < OFF_IPT; ++k) {
+      const int64_t bi = b0 + (int64_t)k * SCAN_THREADS + tid;
+      if (bi < hi) a.offsets[bi] = s_val[pad_l<OFF_IPT>(k * SCAN_THREADS + tid)];
+    }
+    carry += sweep;
+    __syncthreads();  // s_val and s_warp are reused by the next sweep
   }
 }
 

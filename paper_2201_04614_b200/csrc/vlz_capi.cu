@@ -200,16 +200,20 @@ cudaError_t launch_init(vlz_result* res, const WS& w, long long* stats, int64_t 
 }
 
 cudaError_t launch_scan(const ScanArgs& a, cudaStream_t st) {
-  const int64_t nchunks = scan_chunks(a.g.nblocks);
-  const int ipt = scan_ipt(a.g.nblocks);
   const bool t = g_timing.load(std::memory_order_relaxed);
   const int kind = a.gather ? TK_SCAN_C : TK_SCAN_D;
   if (t) timing_mark(kind, true, st);
-  switch (ipt) {
-    case 1: dq_scan_kernel<1><<<(unsigned)nchunks, SCAN_THREADS, 0, st>>>(a); break;
-    case 2: dq_scan_kernel<2><<<(unsigned)nchunks, SCAN_THREADS, 0, st>>>(a); break;
-    case 4: dq_scan_kernel<4><<<(unsigned)nchunks, SCAN_THREADS, 0, st>>>(a); break;
-    default: dq_scan_kernel<8><<<(unsigned)nchunks, SCAN_THREADS, 0, st>>>(a); break;
+  if (a.gather) {
+    const unsigned nchunks = (unsigned)scan_chunks(a.g.nblocks);
+    switch (scan_ipt(a.g.nblocks)) {
+      case 1: dq_scan_kernel<1><<<nchunks, SCAN_THREADS, 0, st>>>(a); break;
+      case 2: dq_scan_kernel<2><<<nchunks, SCAN_THREADS, 0, st>>>(a); break;
+      case 4: dq_scan_kernel<4><<<nchunks, SCAN_THREADS, 0, st>>>(a); break;
+      default: dq_scan_kernel<8><<<nchunks, SCAN_THREADS, 0, st>>>(a); break;
+    }
+  } else {
+    const unsigned nchunks = (unsigned)offsets_chunks(a.g.nblocks);
+    dq_offsets_kernel<<<nchunks, SCAN_THREADS, 0, st>>>(a, offsets_span(a.g.nblocks));
   }
   if (t) timing_mark(kind, false, st);
   g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -349,6 +353,7 @@ __attribute__((visibility("hidden"))) int vlz_internal_compress_begin(const floa
   a.scratch = w.scratch;
   a.counts = d_counts;
   a.scalars = d_scalars;
+  a.origin_vals = reinterpret_cast<float*>(w.offsets);  // offsets are unused by compress
   a.first_nonfinite = reinterpret_cast<unsigned long long*>(&d_result->first_nonfinite);
   a.first_overflow = reinterpret_cast<unsigned long long*>(&d_result->first_overflow);
   a.gsum = reinterpret_cast<unsigned long long*>(stats);
@@ -385,6 +390,7 @@ __attribute__((visibility("hidden"))) int vlz_internal_compress_finish(const flo
   s.fix_origin = mode == MODE_GLOBAL;
   s.gather = 1;
   s.in = d_in;
+  s.origin_vals = reinterpret_cast<const float*>(w.offsets);
   s.codes = d_codes;
   s.counts = d_counts;
   s.scratch = w.scratch;
@@ -448,7 +454,7 @@ __attribute__((visibility("hidden"))) int vlz_internal_decompress(const void* d_
   if (ws_bytes < w.bytes) return VLZ_E_ARG;
   const int mode = mode_of(p->pad_kind, p->pad_gran);
   if (mode != MODE_ZERO && !d_scalars) return VLZ_E_ARG;
-  const int64_t nchunks = scan_chunks(g.nblocks);
+  const int64_t nchunks = offsets_chunks(g.nblocks);
   cudaError_t e = launch_init(d_result, w, nullptr, nchunks, st);
   if (e != cudaSuccess) return to_rc(e);
   const int b = gg->block_edge;
