@@ -51,11 +51,13 @@ struct DFastShape {
   // the ring of interior planes keeps streaming underneath
   static constexpr int EDGE_OFF = DSTAGES * STAGE_BYTES + PREV_BYTES;
   static constexpr int WARP_SMEM = EDGE_OFF + STAGE_BYTES;
+  // per-warp footprint of a kernel variant (the edge slot only when it has edge tiles)
+  __host__ __device__ static constexpr int warp_smem(bool edges) { return edges ? WARP_SMEM : EDGE_OFF; }
 };
 
-template <int ND, int B, int VPL>
+template <int ND, int B, int VPL, bool EDGES = true>
 __host__ __device__ constexpr int dfast_smem_bytes() {
-  return FAST_WARPS * DFastShape<ND, B, VPL>::WARP_SMEM;
+  return FAST_WARPS * DFastShape<ND, B, VPL>::warp_smem(EDGES);
 }
 
 struct DFastArgs {
@@ -436,7 +438,7 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, (EDGES && B == 8) ? 3 : 4)
   extern __shared__ __align__(128) unsigned char smem_dfast[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  unsigned char* ring = smem_dfast + (size_t)wib * F::WARP_SMEM;
+  unsigned char* ring = smem_dfast + (size_t)wib * F::warp_smem(EDGES);
   const Geo& g = fa.d.g;
   const uint16_t* codes = reinterpret_cast<const uint16_t*>(fa.d.codes);
 
@@ -461,21 +463,24 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, (EDGES && B == 8) ? 3 : 4)
 
 // TMA variant (DTProducer): per-warp [stages | previous plane | barriers],
 // 1024-byte aligned for the 128-byte swizzle
-template <int ND, int B, int VPL>
+template <int ND, int B, int VPL, bool EDGES>
 struct DTmaShape {
   using F = DFastShape<ND, B, VPL>;
-  static constexpr int BAR_OFF = F::WARP_SMEM;  // stages | previous plane | edge slot
+  static constexpr int BAR_OFF = F::warp_smem(EDGES);  // stages | previous plane [| edge slot]
   static constexpr int WARP_SMEM = (BAR_OFF + 64 + 1023) / 1024 * 1024;
 };
-template <int ND, int B, int VPL>
+template <int ND, int B, int VPL, bool EDGES>
 __host__ __device__ constexpr int dtma_smem_bytes() {
-  return FAST_WARPS * DTmaShape<ND, B, VPL>::WARP_SMEM + 1024;
+  return FAST_WARPS * DTmaShape<ND, B, VPL, EDGES>::WARP_SMEM + 1024;
 }
 
+#ifndef VLZ_DTMA_MINB
+#define VLZ_DTMA_MINB 5  // CTAs per SM of the lean TMA decompress kernel (95 regs, no spills; 4: 102 regs, 6: spills)
+#endif
 template <int ND, int B, int VPL, bool EDGES>
-__global__ void __launch_bounds__(FAST_WARPS * 32, (EDGES && B == 8) ? 3 : 4)
+__global__ void __launch_bounds__(FAST_WARPS * 32, EDGES ? 3 : VLZ_DTMA_MINB)
     dq_decompress_tma_kernel(const __grid_constant__ DFastArgs fa) {
-  using T = DTmaShape<ND, B, VPL>;
+  using T = DTmaShape<ND, B, VPL, EDGES>;
   extern __shared__ __align__(1024) unsigned char smem_dtma[];
   // align by an offset from the shared array itself (keeps the accesses LDS/STS)
   unsigned char* base = smem_dtma + ((1024u - (smem_u32(smem_dtma) & 1023u)) & 1023u);

@@ -45,14 +45,14 @@ static cudaError_t run_d(bool u32, const DecompressArgs& a, cudaStream_t st) {
       const bool edges = edge_tile_count<ND, B, VPL>(a.g) > 0;
       auto kern = edges ? dq_decompress_fast_kernel<ND, B, VPL, true>
                         : dq_decompress_fast_kernel<ND, B, VPL, false>;
-      int fsmem = dfast_smem_bytes<ND, B, VPL>();
+      int fsmem = edges ? dfast_smem_bytes<ND, B, VPL, true>() : dfast_smem_bytes<ND, B, VPL, false>();
       if constexpr (ND == 3 && B == 8 && VPL == 4) {
         // every block full (block b starts at b * 512): TMA tensor loads
         if (a.g.D0 % 8 == 0 && a.g.D1 % 8 == 0 && a.g.D2 % 8 == 0 &&
             a.g.nblocks < (1ll << 31) && make_code_map(&fa.tmap, a.codes, a.g.nblocks)) {
           kern = edges ? dq_decompress_tma_kernel<ND, B, VPL, true>
                        : dq_decompress_tma_kernel<ND, B, VPL, false>;
-          fsmem = dtma_smem_bytes<ND, B, VPL>();
+          fsmem = edges ? dtma_smem_bytes<ND, B, VPL, true>() : dtma_smem_bytes<ND, B, VPL, false>();
         }
       }
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem);
