@@ -16,7 +16,7 @@
  *    reported in a caller-allocated device `vlz_result` the caller reads back.
  *  - return value: VLZ_OK or a launch/argument error (VLZ_E_ARG, VLZ_E_CUDA).
  *  - the library allocates nothing on the device paths (workspace is caller
- *    owned); the *_host paths keep a per-device cache of staging buffers.
+ *    owned); the *_host paths keep a per-device pool of staging buffers.
  */
 #ifndef VLZ_GPU_H_
 #define VLZ_GPU_H_
@@ -150,7 +150,10 @@ int vlz_minmax(const float* d_in, int64_t n, double* d_minmax, void* stream);
 /* ---- host-buffer entry points (end-to-end: H2D + kernels + D2H) -------- *
  * Same semantics as the device versions; buffers are host memory (pinned for
  * full PCIe speed).  Synchronous: returns after the results are in host
- * memory.  *h_result receives the status block. */
+ * memory.  *h_result receives the status block.  Thread-safe: concurrent
+ * calls (up to 4 per device) run on their own streams and staging buffers,
+ * so a compress (mostly H2D) and a decompress (mostly D2H) issued from two
+ * host threads overlap on the full-duplex link. */
 int vlz_dq_compress_host(const float* h_in, const vlz_geom* g, const vlz_params* p,
                          uint16_t* h_codes, float* h_outliers, int64_t* h_counts,
                          int64_t* h_scalars, vlz_result* h_result, int device);

@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <condition_variable>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -84,11 +85,63 @@ struct Ctx {
   void* buf = nullptr;
   size_t cap = 0;
   std::vector<cudaEvent_t> ev;
+  // pinned host scratch for the small result/statistics/patch transfers: a
+  // copy to or from pageable memory is synchronous inside the driver and
+  // stalls the CUDA calls of concurrent host threads
+  void* hbuf = nullptr;
+  size_t hcap = 0;
+  bool busy = false;
 };
-Ctx g_ctx[64];
+// Per device, a small pool of contexts (streams + device buffer): concurrent
+// calls from different host threads each take their own context, so e.g. a
+// compress (mostly host->device traffic) and a decompress (mostly
+// device->host) overlap on the full-duplex link.  A call holds its context
+// for its whole duration; the pool grows on demand up to kPool contexts.
+constexpr int kPool = 4;
+Ctx g_ctx[64][kPool];
 std::mutex g_mu;
+std::condition_variable g_cv;
 
-bool ensure(Ctx& c, size_t need, size_t nev) {
+Ctx* acquire(int device) {
+  std::unique_lock<std::mutex> lk(g_mu);
+  for (;;) {
+    for (Ctx& c : g_ctx[device])
+      if (!c.busy) {
+        c.busy = true;
+        return &c;
+      }
+    g_cv.wait(lk);
+  }
+}
+void release(Ctx* c) {
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    c->busy = false;
+  }
+  g_cv.notify_all();
+}
+// RAII: context + current device for the duration of one call
+struct Lease {
+  Ctx* cx;
+  int prev = 0;
+  explicit Lease(int device) : cx(acquire(device)) {
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+  }
+  ~Lease() {
+    // nothing of this call may still be in flight when the context is reused
+    // (early error returns leave copies queued)
+    if (cx->h2d) {
+      cudaStreamSynchronize(cx->h2d);
+      cudaStreamSynchronize(cx->comp);
+      cudaStreamSynchronize(cx->d2h);
+    }
+    cudaSetDevice(prev);
+    release(cx);
+  }
+};
+
+bool ensure(Ctx& c, size_t need, size_t nev, size_t hneed) {
   if (!c.h2d) {
     cudaStreamCreateWithFlags(&c.h2d, cudaStreamNonBlocking);
     cudaStreamCreateWithFlags(&c.comp, cudaStreamNonBlocking);
@@ -100,6 +153,13 @@ bool ensure(Ctx& c, size_t need, size_t nev) {
     c.cap = 0;
     if (cudaMalloc(&c.buf, need) != cudaSuccess) return false;
     c.cap = need;
+  }
+  if (c.hcap < hneed) {
+    if (c.hbuf) cudaFreeHost(c.hbuf);
+    c.hbuf = nullptr;
+    c.hcap = 0;
+    if (cudaHostAlloc(&c.hbuf, hneed, cudaHostAllocDefault) != cudaSuccess) return false;
+    c.hcap = hneed;
   }
   while (c.ev.size() < nev) {
     cudaEvent_t e;
@@ -145,15 +205,18 @@ int vlz_dq_compress_host(const float* h_in, const vlz_geom* gg, const vlz_params
                o_res = o_sc + a256((ns > 0 ? ns : 1) * 8), o_st = o_res + a256(nc * 64),
                o_pc = o_st + a256((nc + 1) * 32), o_pl = o_pc + a256(nc * 4),
                o_ws = o_pl + a256(nb_total * 8), total = o_ws + wsum;
-  std::lock_guard<std::mutex> lk(g_mu);
-  int prev = 0;
-  cudaGetDevice(&prev);
-  cudaSetDevice(device);
-  Ctx& cx = g_ctx[device];
-  if (!ensure(cx, total, 2 * nc + 2)) {
-    cudaSetDevice(prev);
-    return VLZ_E_CUDA;
-  }
+  // pinned host scratch: results | statistics | reduced statistics | patch counts | patches
+  const size_t h_res = 0, h_st = a256(nc * 64), h_red = h_st + a256(nc * 32),
+               h_np = h_red + 256, h_pl = h_np + a256(nc * 4), htotal = h_pl + a256(nb_total * 8);
+  Lease lease(device);
+  Ctx& cx = *lease.cx;
+  if (!ensure(cx, total, 2 * nc + 2, htotal)) return VLZ_E_CUDA;
+  char* hbase = static_cast<char*>(cx.hbuf);
+  vlz_result* res = reinterpret_cast<vlz_result*>(hbase + h_res);
+  long long* st = reinterpret_cast<long long*>(hbase + h_st);
+  long long* red = reinterpret_cast<long long*>(hbase + h_red);
+  unsigned int* npatch = reinterpret_cast<unsigned int*>(hbase + h_np);
+  unsigned long long* patches = reinterpret_cast<unsigned long long*>(hbase + h_pl);
   char* base = static_cast<char*>(cx.buf);
   float* d_in = reinterpret_cast<float*>(base + o_in);
   uint16_t* d_codes = reinterpret_cast<uint16_t*>(base + o_codes);
@@ -191,13 +254,14 @@ int vlz_dq_compress_host(const float* h_in, const vlz_geom* gg, const vlz_params
     cudaMemcpyAsync(h_codes + c.elem_off, d_codes + c.elem_off, c.n * 2, cudaMemcpyDeviceToHost,
                     cx.d2h);
   }
-  std::vector<vlz_result> res(nc);
   if (rc == VLZ_OK && global) {
     // all-reduce of the chunks' statistics (as across ranks), then finish
-    std::vector<long long> st(4 * nc);
-    cudaMemcpyAsync(st.data(), d_st, 32 * nc, cudaMemcpyDeviceToHost, cx.comp);
+    cudaMemcpyAsync(st, d_st, 32 * nc, cudaMemcpyDeviceToHost, cx.comp);
     rc = rc_of(cudaStreamSynchronize(cx.comp));
-    long long red[4] = {0, 0, st[2], st[3]};
+    red[0] = 0;
+    red[1] = 0;
+    red[2] = st[2];
+    red[3] = st[3];
     unsigned long long usum = 0;
     for (size_t i = 0; i < nc; ++i) {
       usum += (unsigned long long)st[4 * i];
@@ -215,7 +279,6 @@ int vlz_dq_compress_host(const float* h_in, const vlz_geom* gg, const vlz_params
                                         d_res + i, base + ws_off[i], c.ws_bytes, cx.comp,
                                         d_pl + c.block_off, d_pc + i);
     }
-    cudaStreamSynchronize(cx.comp);  // red[] lives on this stack frame
   }
   if (rc == VLZ_OK) {
     cudaEvent_t done = cx.ev[2 * nc];
@@ -223,9 +286,8 @@ int vlz_dq_compress_host(const float* h_in, const vlz_geom* gg, const vlz_params
     cudaStreamWaitEvent(cx.d2h, done, 0);
     cudaMemcpyAsync(h_counts, d_cnt, nb_total * 8, cudaMemcpyDeviceToHost, cx.d2h);
     if (ns > 0) cudaMemcpyAsync(h_scalars, d_sc, ns * 8, cudaMemcpyDeviceToHost, cx.d2h);
-    cudaMemcpyAsync(res.data(), d_res, 64 * nc, cudaMemcpyDeviceToHost, cx.d2h);
-    std::vector<unsigned int> npatch(nc, 0);
-    cudaMemcpyAsync(npatch.data(), d_pc, 4 * nc, cudaMemcpyDeviceToHost, cx.d2h);
+    cudaMemcpyAsync(res, d_res, 64 * nc, cudaMemcpyDeviceToHost, cx.d2h);
+    cudaMemcpyAsync(npatch, d_pc, 4 * nc, cudaMemcpyDeviceToHost, cx.d2h);
     rc = rc_of(cudaStreamSynchronize(cx.d2h));
     // combine: first non-finite index anywhere, else first overflow index
     vlz_result out{};
@@ -260,13 +322,11 @@ int vlz_dq_compress_host(const float* h_in, const vlz_geom* gg, const vlz_params
       }
       // origins the *:global finish rewrote after the provisional codes left:
       // chunk i's patches sit at d_pl + block_off_i as (chunk position << 16 | code)
-      std::vector<unsigned long long> patches;
       std::vector<size_t> pstart(nc + 1, 0);
       for (size_t i = 0; i < nc; ++i) pstart[i + 1] = pstart[i] + npatch[i];
-      patches.resize(pstart[nc]);
       for (size_t i = 0; i < nc; ++i)
         if (npatch[i])
-          cudaMemcpyAsync(patches.data() + pstart[i], d_pl + ch[i].block_off, 8ull * npatch[i],
+          cudaMemcpyAsync(patches + pstart[i], d_pl + ch[i].block_off, 8ull * npatch[i],
                           cudaMemcpyDeviceToHost, cx.d2h);
       rc = rc_of(cudaStreamSynchronize(cx.d2h));
       for (size_t i = 0; i < nc && rc == VLZ_OK; ++i)
@@ -274,7 +334,6 @@ int vlz_dq_compress_host(const float* h_in, const vlz_geom* gg, const vlz_params
           h_codes[ch[i].elem_off + (int64_t)(patches[k] >> 16)] = (uint16_t)(patches[k] & 0xffff);
     }
   }
-  cudaSetDevice(prev);
   return rc;
 }
 
@@ -312,15 +371,10 @@ int vlz_dq_decompress_host(const uint16_t* h_codes, const float* h_outliers, int
   const size_t o_codes = 0, o_ol = a256(N * 2), o_cnt = o_ol + a256(n_outliers * 4 + 4),
                o_sc = o_cnt + a256(nb_total * 8), o_out = o_sc + a256((ns > 0 ? ns : 1) * 8),
                o_res = o_out + a256(N * 4), o_ws = o_res + a256(nc * 64), total = o_ws + wsum;
-  std::lock_guard<std::mutex> lk(g_mu);
-  int prev = 0;
-  cudaGetDevice(&prev);
-  cudaSetDevice(device);
-  Ctx& cx = g_ctx[device];
-  if (!ensure(cx, total, 2 * nc + 2)) {
-    cudaSetDevice(prev);
-    return VLZ_E_CUDA;
-  }
+  Lease lease(device);
+  Ctx& cx = *lease.cx;
+  if (!ensure(cx, total, 2 * nc + 2, a256(nc * 64))) return VLZ_E_CUDA;
+  vlz_result* res = static_cast<vlz_result*>(cx.hbuf);  // pinned
   char* base = static_cast<char*>(cx.buf);
   uint16_t* d_codes = reinterpret_cast<uint16_t*>(base + o_codes);
   float* d_ol = reinterpret_cast<float*>(base + o_ol);
@@ -351,11 +405,10 @@ int vlz_dq_decompress_host(const uint16_t* h_codes, const float* h_outliers, int
     cudaMemcpyAsync(h_out + c.elem_off, d_out + c.elem_off, c.n * 4, cudaMemcpyDeviceToHost,
                     cx.d2h);
   }
-  std::vector<vlz_result> res(nc);
   if (rc == VLZ_OK) {
     cudaEventRecord(cx.ev[2 * nc], cx.comp);
     cudaStreamWaitEvent(cx.d2h, cx.ev[2 * nc], 0);
-    cudaMemcpyAsync(res.data(), d_res, 64 * nc, cudaMemcpyDeviceToHost, cx.d2h);
+    cudaMemcpyAsync(res, d_res, 64 * nc, cudaMemcpyDeviceToHost, cx.d2h);
     rc = rc_of(cudaStreamSynchronize(cx.d2h));
   }
   if (rc == VLZ_OK) {
@@ -394,17 +447,22 @@ int vlz_dq_decompress_host(const uint16_t* h_codes, const float* h_outliers, int
       }
     }
   }
-  cudaSetDevice(prev);
   return rc;
 }
 
 void vlz_host_release(void) {
-  std::lock_guard<std::mutex> lk(g_mu);
-  for (auto& c : g_ctx) {
-    if (c.buf) cudaFree(c.buf);
-    c.buf = nullptr;
-    c.cap = 0;
-  }
+  std::unique_lock<std::mutex> lk(g_mu);
+  for (auto& dev : g_ctx)
+    for (Ctx& c : dev) {
+      // wait for a call still holding this context
+      g_cv.wait(lk, [&] { return !c.busy; });
+      if (c.buf) cudaFree(c.buf);
+      if (c.hbuf) cudaFreeHost(c.hbuf);
+      c.buf = nullptr;
+      c.cap = 0;
+      c.hbuf = nullptr;
+      c.hcap = 0;
+    }
 }
 
 }  // extern "C"

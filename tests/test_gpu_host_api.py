@@ -102,3 +102,50 @@ def test_host_decompress_reports_first_failing_block():
     grid = M.build_block_grid(M.ArrayDescriptor(3, d.shape), 8)
     with pytest.raises(CorruptStreamError):
         reconstruct_arrays(hc, ho, bad, hs, grid, eb, 512, M.PaddingPolicy.parse("mean:block"))
+
+
+def test_host_calls_from_concurrent_threads():
+    """Compress and decompress issued from several host threads at once (each
+    on its own pooled context) give exactly the serial results."""
+    import threading
+
+    d = workloads.gen_c3(shape=(96, 64, 128)) + np.float32(11.5)
+    eb = workloads.value_range_eb(d, 1e-4)
+    hc, ho, hn, hs, _ = _host_compress(d, eb, 8, "mean:global", 512)
+    lib = _lib.load()
+    g = _lib.geom(d.shape, 8)
+    pr = _lib.params(eb, 512, 3, 0)
+    want = np.empty(d.shape, np.float32)
+    rd = _lib.Result()
+    assert lib.vlz_dq_decompress_host(hc.ctypes.data, ho.ctypes.data, ho.size, hn.ctypes.data,
+                                      hs.ctypes.data, ctypes.byref(g), ctypes.byref(pr),
+                                      want.ctypes.data, ctypes.byref(rd), 0) == 0
+    errs = []
+
+    def worker(k):
+        try:
+            for _ in range(3):
+                if k % 2 == 0:
+                    c2, o2, n2, s2, r2 = _host_compress(d, eb, 8, "mean:global", 512)
+                    assert r2.status == 0
+                    assert c2.tobytes() == hc.tobytes() and o2.tobytes() == ho.tobytes()
+                    assert n2.tobytes() == hn.tobytes() and s2.tobytes() == hs.tobytes()
+                else:
+                    out = np.empty(d.shape, np.float32)
+                    r3 = _lib.Result()
+                    rc = lib.vlz_dq_decompress_host(hc.ctypes.data, ho.ctypes.data, ho.size,
+                                                    hn.ctypes.data, hs.ctypes.data,
+                                                    ctypes.byref(g), ctypes.byref(pr),
+                                                    out.ctypes.data, ctypes.byref(r3), 0)
+                    assert rc == 0 and r3.status == 0
+                    assert out.tobytes() == want.tobytes()
+        except BaseException as e:  # reported below
+            errs.append(e)
+
+    th = [threading.Thread(target=worker, args=(k,)) for k in range(6)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    lib.vlz_host_release()
+    assert not errs, errs[0]

@@ -15,7 +15,7 @@ from paper_2201_04614_b200.padding import outlier_report  # noqa: E402
 
 rng = np.random.default_rng(0)
 cases = [((64,), 8), ((1000,), 64), ((24, 40), 8), ((36, 72), 16), ((16, 16, 256), 8),
-         ((13, 21, 132), 8), ((16, 32, 64), 16), ((9, 20, 30), 8)]
+         ((13, 21, 132), 8), ((16, 32, 64), 16), ((9, 20, 30), 8), ((48, 64, 128), 8)]
 for shape, b in cases:
     idx = np.indices(shape).astype(np.float64)
     data = sum(np.sin(0.1 * (k + 1) * idx[k]) * 30 for k in range(len(shape)))
