@@ -475,7 +475,8 @@ __host__ __device__ constexpr int dtma_smem_bytes() {
 }
 
 #ifndef VLZ_DTMA_MINB
-#define VLZ_DTMA_MINB 5  // CTAs per SM of the lean TMA decompress kernel (95 regs, no spills; 4: 102 regs, 6: spills)
+#define VLZ_DTMA_MINB 4  // CTAs per SM of the lean TMA decompress kernel (102 regs; 5 CTAs at 95 regs measured
+                         // -1.7 % on one box and +3 % on two others, 6 spills)
 #endif
 template <int ND, int B, int VPL, bool EDGES>
 __global__ void __launch_bounds__(FAST_WARPS * 32, EDGES ? 3 : VLZ_DTMA_MINB)
