@@ -11,7 +11,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libvlzgpu.so")
+LIB_PATH = os.environ.get("VLZ_LIB") or os.path.join(_HERE, "libvlzgpu.so")  # VLZ_LIB: A/B runs of two builds
 
 
 class Geom(ctypes.Structure):

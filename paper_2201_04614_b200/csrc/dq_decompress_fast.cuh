@@ -231,7 +231,7 @@ __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, c
     }
   }
   int run = 0;
-  bool badcode = false;
+  unsigned cmax_run = 0u;  // running max of the tile's codes (>= 2R: corrupt stream)
   int dmax = 0, dmin = 0;  // range of every d of the tile (exact iff within +-2^27)
   float* orow = a.out + (z0 * g.D1 + y0) * g.D2 + xl0;
   const unsigned char* const slot0 = ring + (EDGE ? F::EDGE_OFF : 0) + lane * F::LANE_BYTES;
@@ -297,14 +297,15 @@ __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, c
 #pragma unroll
         for (int j = 0; j < VPL; ++j) ep[j] = 0;
       }
-      bool anysent = false;
-      unsigned cmax = c[0];
+      // sentinel test by a min over the row's codes; the code-range check
+      // only keeps a running max, tested once per tile
+      unsigned cmin = c[0];
 #pragma unroll
       for (int j = 0; j < VPL; ++j) {
-        anysent = anysent || (c[j] == 0u);
-        cmax = c[j] > cmax ? c[j] : cmax;
+        cmin = c[j] < cmin ? c[j] : cmin;
+        cmax_run = c[j] > cmax_run ? c[j] : cmax_run;
       }
-      badcode |= cmax >= (unsigned)(2 * R);
+      const bool anysent = cmin == 0u;
       int h[VPL];
       unsigned smask = 0;
       float vs[VPL];
@@ -417,7 +418,7 @@ __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, c
     if (lane == 0) fa.redo_list[atomicAdd(fa.redo_count, 1u)] = tile;
     return;
   }
-  const bool bad_any = group_any<LPB>(badcode, lane);
+  const bool bad_any = group_any<LPB>(cmax_run >= (unsigned)(2 * R), lane);
   if (xin == 0 && bvalid) {
     sent_acc += run;
     int st = 0;
