@@ -34,6 +34,10 @@
 
 namespace vlz {
 
+#ifndef VLZ_DQ_I2F
+#define VLZ_DQ_I2F 0  // 1: int->double by I2F.F64 instead of the magic-number DADD
+#endif
+
 // ring depth of the decompress producers (planes in flight per warp)
 constexpr int DSTAGES = 2;
 
@@ -307,6 +311,7 @@ __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, c
       }
       const bool anysent = cmin == 0u;
       int h[VPL];
+      int pvc = 0;  // carry from earlier lanes not yet in h (common path)
       unsigned smask = 0;
       float vs[VPL];
       if (!__any_sync(FULL, anysent)) {
@@ -320,9 +325,7 @@ __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, c
           const int u = __shfl_up_sync(FULL, inc, o);
           if (gl >= o) inc += u;
         }
-        const int pv = inc - h[VPL - 1];  // exclusive carry from earlier lanes
-#pragma unroll
-        for (int j = 0; j < VPL; ++j) h[j] += pv;
+        pvc = inc - h[VPL - 1];  // exclusive carry, added with grow below (one IADD3)
       } else {
         // rare: sentinels reset the scan to d_s - E'(prev plane) - G(prev row)
 #pragma unroll
@@ -371,13 +374,17 @@ __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, c
       int dv[VPL];
 #pragma unroll
       for (int j = 0; j < VPL; ++j) {
-        const int gv = h[j] + grow[j];
+        const int gv = h[j] + grow[j] + pvc;
         grow[j] = gv;
         dv[j] = gv + ep[j];  // = d (primed state)
+#if VLZ_DQ_I2F
+        const double dd = (double)dv[j];
+#else
         // float64(d) without the quarter-rate I2F: 2^52 + 2^31 + d has d in
         // its low word exactly, one DADD removes the offset (exact)
         const double dd = __dadd_rn(__hiloint2double(0x43300000, dv[j] ^ (int)0x80000000),
                                     -4503601774854144.0);
+#endif
         o[j] = __double2float_rn(__dmul_rn(dd, a.q.twoeb));
       }
 #pragma unroll

@@ -1,11 +1,11 @@
 #!/bin/bash
-# A/B of two prebuilt libraries on one GPU box, interleaved A B A B:
-#   bash tools/ab_lib.sh TAG path/to/libA.so path/to/libB.so [reps]
-TAG=$1; A=$2; B=$3; REPS=${4:-3}
+# A/B/... of prebuilt libraries on one GPU box, interleaved (A B C A B C ...):
+#   bash tools/ab_lib.sh TAG REPS lib1.so lib2.so [lib3.so ...]
+TAG=$1; REPS=$2; shift 2
 O=gpurun_out/$TAG; mkdir -p $O
 for rep in $(seq $REPS); do
-  for v in A B; do
-    lib=$A; [ $v = B ] && lib=$B
+  for lib in "$@"; do
+    v=$(basename $lib .so)
     VLZ_LIB=$(realpath $lib) python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > $O/bench_${v}_$rep.json 2>>$O/bench.err
   done
 done
