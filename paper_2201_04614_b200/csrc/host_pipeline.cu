@@ -16,6 +16,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <thread>
+#include <cstdlib>
 #include <condition_variable>
 #include <cstring>
 #include <mutex>
@@ -41,7 +45,15 @@ int vlz_internal_decompress(const void* d_codes, bool u32, const float* d_outlie
 
 namespace {
 
-constexpr size_t kChunkBytes = size_t(64) << 20;  // ~64 MB of float32 per chunk
+// ~64 MB of float32 per chunk (VLZ_CHUNK_MB overrides, for tuning runs)
+size_t chunk_bytes() {
+  static const size_t v = [] {
+    const char* e = std::getenv("VLZ_CHUNK_MB");
+    const long mb = e ? std::atol(e) : 0;
+    return size_t(mb > 0 ? mb : 64) << 20;
+  }();
+  return v;
+}
 
 size_t a256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -61,7 +73,7 @@ std::vector<Chunk> plan(const vlz_geom* gg) {
   for (int d = 1; d < gg->nd; ++d) blocks_per_layer *= (gg->dims[d] + b - 1) / b;
   const int64_t layers = (gg->dims[0] + b - 1) / b;
   const int64_t layer_bytes = (int64_t)b * plane * 4;
-  int64_t per = (int64_t)(kChunkBytes / (size_t)std::max<int64_t>(layer_bytes, 1));
+  int64_t per = (int64_t)(chunk_bytes() / (size_t)std::max<int64_t>(layer_bytes, 1));
   if (per < 1) per = 1;
   std::vector<Chunk> out;
   for (int64_t l0 = 0; l0 < layers; l0 += per) {
@@ -176,6 +188,15 @@ int64_t scalars_at(const vlz_params* p, int nd, int64_t block_off) {
 
 int rc_of(cudaError_t e) { return e == cudaSuccess ? VLZ_OK : VLZ_E_CUDA; }
 
+// VLZ_HOST_PROFILE=1: phase times of the host entry points on stderr
+bool host_profile() {
+  static const bool v = std::getenv("VLZ_HOST_PROFILE") != nullptr;
+  return v;
+}
+double ms_since(std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+  return std::chrono::duration<double, std::milli>(b - a).count();
+}
+
 }  // namespace
 
 extern "C" {
@@ -189,6 +210,7 @@ int vlz_dq_compress_host(const float* h_in, const vlz_geom* gg, const vlz_params
     return VLZ_E_ARG;
   const int64_t ns = vlz_scalar_count(gg, p->pad_kind, p->pad_gran);
   if (ns > 0 && !h_scalars) return VLZ_E_ARG;
+  const auto t_start = std::chrono::steady_clock::now();
   std::vector<Chunk> ch = plan(gg);
   const size_t nc = ch.size();
   int64_t N = 0, wsum = 0;
@@ -329,9 +351,26 @@ int vlz_dq_compress_host(const float* h_in, const vlz_geom* gg, const vlz_params
           cudaMemcpyAsync(patches + pstart[i], d_pl + ch[i].block_off, 8ull * npatch[i],
                           cudaMemcpyDeviceToHost, cx.d2h);
       rc = rc_of(cudaStreamSynchronize(cx.d2h));
-      for (size_t i = 0; i < nc && rc == VLZ_OK; ++i)
-        for (size_t k = pstart[i]; k < pstart[i + 1]; ++k)
-          h_codes[ch[i].elem_off + (int64_t)(patches[k] >> 16)] = (uint16_t)(patches[k] & 0xffff);
+      const auto tp = std::chrono::steady_clock::now();
+      // chunks patch disjoint code ranges: spread them over a few host threads
+      auto apply = [&](size_t i0, size_t i1) {
+        for (size_t i = i0; i < i1; ++i)
+          for (size_t k = pstart[i]; k < pstart[i + 1]; ++k)
+            h_codes[ch[i].elem_off + (int64_t)(patches[k] >> 16)] =
+                (uint16_t)(patches[k] & 0xffff);
+      };
+      if (rc == VLZ_OK) {
+        const size_t nth = std::min<size_t>(
+            {nc, (size_t)8, (size_t)std::max(1u, std::thread::hardware_concurrency() / 2),
+             (size_t)std::max<size_t>(1, pstart[nc] / 65536)});
+        std::vector<std::thread> th;
+        for (size_t t = 1; t < nth; ++t) th.emplace_back(apply, nc * t / nth, nc * (t + 1) / nth);
+        apply(0, nc / nth);
+        for (auto& x : th) x.join();
+      }
+      if (host_profile())
+        std::fprintf(stderr, "[vlz host] compress %zu chunks: %.2f ms to results, patches %zu in %.2f ms\n",
+                     nc, ms_since(t_start, tp), (size_t)pstart[nc], ms_since(tp, std::chrono::steady_clock::now()));
     }
   }
   return rc;
