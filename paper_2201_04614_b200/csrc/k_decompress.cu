@@ -107,7 +107,7 @@ cudaError_t launch_decompress(int nd, int B, bool u32, const DecompressArgs& a, 
   } else if (nd == 3) {
     switch (B) {
       case 8: return run_d<3, 8, VLZ_VPL_3D8>(u32, a, st);
-      case 16: return run_d<3, 16, 2>(u32, a, st);
+      case 16: return run_d<3, 16, VLZ_DVPL_3D16>(u32, a, st);
       case 32: return run_d<3, 32, 4>(u32, a, st);
       case 64: return run_d<3, 64, 2>(u32, a, st);
     }

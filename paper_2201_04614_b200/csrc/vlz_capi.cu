@@ -323,10 +323,12 @@ int64_t vlz_scalar_count(const vlz_geom* gg, int32_t kind, int32_t gran) {
 }
 
 size_t vlz_workspace_size(const vlz_geom* gg) {
-  Geo g;
-  if (!make_geo(gg, g)) return 0;
+  // large enough for both directions (their tile windows may differ)
+  Geo gd, gc;
+  if (!make_geo(gg, gd) || !make_geo(gg, gc, true)) return 0;
   char* null_base = nullptr;
-  return carve(g, null_base).bytes;
+  const size_t d = carve(gd, null_base).bytes, c = carve(gc, null_base).bytes;
+  return d > c ? d : c;
 }
 
 __attribute__((visibility("hidden"))) int vlz_internal_compress_begin(const float* d_in, const vlz_geom* gg, const vlz_params* p,
