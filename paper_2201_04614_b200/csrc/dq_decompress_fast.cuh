@@ -342,7 +342,12 @@ __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, c
           if ((smask >> j) & 1u) {
             if (k < avail) vs[j] = a.outliers[off + k];
             ++k;
-            const long long ds = quant_value(vs[j], a.q.twoeb);
+            // the compress side's exact-fast quotient (quant_fast: equal to
+            // round_half_away(fl64(v / 2eb)) whenever it reports ok); the fp64
+            // division only for the rest
+            bool qok;
+            const int nq = quant_fast(vs[j], a.q, qok);
+            const long long ds = qok ? (long long)nq : quant_value(vs[j], a.q.twoeb);
             wide |= (ds >= (1ll << 27)) || (ds <= -(1ll << 27));
             acc = (int)ds - ep[j] - grow[j];
             reset = true;
