@@ -1,0 +1,132 @@
+// k_1d.cu -- launch of the fused 1-D kernels (dq_1d.cuh) + their int64 redo.
+#include "dq_1d.cuh"
+#include "launch.cuh"
+
+namespace vlz {
+
+template <typename Kern>
+static cudaError_t d1_grid(Kern kern, int smem, int64_t ntiles1, int64_t& grid) {
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, D1_WARPS * 32, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  grid = (int64_t)per_sm * num_sms();
+  const int64_t need = (ntiles1 + D1_WARPS - 1) / D1_WARPS;
+  if (grid > need) grid = need;
+  if (grid < 1) grid = 1;
+  return cudaSuccess;
+}
+
+template <int B, int MODE, int K>
+static cudaError_t run_c1d(const CompressArgs& a, cudaStream_t st) {
+  D1Args fa{};
+  fa.c = a;
+  fa.redo_count = const_cast<unsigned int*>(a.redo_count);
+  fa.redo_list = const_cast<long long*>(a.redo_list);
+  auto kern = dq_compress_1d_kernel<B, MODE, K>;
+  constexpr int smem = D1_WARPS * d1_warp_smem<4>();
+  int64_t grid = 0;
+  cudaError_t e = d1_grid(kern, smem, (a.g.D2 + D1_TILE - 1) / D1_TILE, grid);
+  if (e != cudaSuccess) return e;
+  const bool t = g_timing.load(std::memory_order_relaxed);
+  if (t) timing_mark(TK_COMPRESS, true, st);
+  kern<<<(unsigned)grid, D1_WARPS * 32, smem, st>>>(fa);
+  if (t) timing_mark(TK_COMPRESS, false, st);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  // int64 redo of the rows whose |d| reached 2^30 (usually none: exits at once)
+  constexpr int VG = B == 256 ? 8 : 4;
+  auto redo = dq_compress_kernel<1, B, VG, MODE, true>;
+  constexpr int psmem = 4 * plane_smem_bytes<1, B, VG>();
+  if (t) timing_mark(TK_REDO, true, st);
+  redo<<<(unsigned)num_sms(), 128, psmem, st>>>(a);
+  if (t) timing_mark(TK_REDO, false, st);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+template <int B, int MODE>
+static cudaError_t run_c1d_k(const CompressArgs& a, cudaStream_t st) {
+  if (MODE == MODE_ZERO) return run_c1d<B, MODE, 0>(a, st);
+  if (a.q.kind == 1) return run_c1d<B, MODE, 1>(a, st);
+  if (a.q.kind == 2) return run_c1d<B, MODE, 2>(a, st);
+  return run_c1d<B, MODE, 3>(a, st);
+}
+
+template <int B>
+static cudaError_t run_c1d_b(int mode, const CompressArgs& a, cudaStream_t st) {
+  switch (mode) {
+    case MODE_ZERO: return run_c1d_k<B, MODE_ZERO>(a, st);
+    case MODE_GLOBAL: return run_c1d_k<B, MODE_GLOBAL>(a, st);
+    case MODE_BLOCK: return run_c1d_k<B, MODE_BLOCK>(a, st);
+    default: return run_c1d_k<B, MODE_EDGE>(a, st);
+  }
+}
+
+bool d1_fast_compress_ok(const CompressArgs& a) {
+  return a.redo_list != nullptr && (reinterpret_cast<uintptr_t>(a.in) & 15) == 0 &&
+         (reinterpret_cast<uintptr_t>(a.codes) & 15) == 0 && a.g.D2 < (1ll << 40) &&
+         (a.g.D2 + D1_TILE - 1) / D1_TILE < (1ll << 31);
+}
+
+cudaError_t launch_compress_1d(int B, int mode, const CompressArgs& a, cudaStream_t st) {
+  switch (B) {
+    case 8: return run_c1d_b<8>(mode, a, st);
+    case 16: return run_c1d_b<16>(mode, a, st);
+    case 32: return run_c1d_b<32>(mode, a, st);
+    case 64: return run_c1d_b<64>(mode, a, st);
+    case 256: return run_c1d_b<256>(mode, a, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <int B>
+static cudaError_t run_d1d(const DecompressArgs& a, cudaStream_t st) {
+  D1Args fa{};
+  fa.d = a;
+  fa.redo_count = const_cast<unsigned int*>(a.redo_count);
+  fa.redo_list = const_cast<long long*>(a.redo_list);
+  auto kern = dq_decompress_1d_kernel<B>;
+  constexpr int smem = D1_WARPS * d1_warp_smem<2>();
+  int64_t grid = 0;
+  cudaError_t e = d1_grid(kern, smem, (a.g.D2 + D1_TILE - 1) / D1_TILE, grid);
+  if (e != cudaSuccess) return e;
+  const bool t = g_timing.load(std::memory_order_relaxed);
+  if (t) timing_mark(TK_DECOMPRESS, true, st);
+  kern<<<(unsigned)grid, D1_WARPS * 32, smem, st>>>(fa);
+  if (t) timing_mark(TK_DECOMPRESS, false, st);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  // int64 redo of flagged rows; its last CTA also settles the status
+  constexpr int VG = B == 256 ? 8 : 4;
+  auto redo = dq_decompress_kernel<1, B, VG, uint16_t, true>;
+  constexpr int psmem = 4 * plane_smem_bytes<1, B, VG>();
+  if (t) timing_mark(TK_REDO, true, st);
+  redo<<<(unsigned)num_sms() * 2, 128, psmem, st>>>(a);
+  if (t) timing_mark(TK_REDO, false, st);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+bool d1_fast_decompress_ok(bool u32, const DecompressArgs& a) {
+  return !u32 && a.redo_list != nullptr && (reinterpret_cast<uintptr_t>(a.codes) & 15) == 0 &&
+         (reinterpret_cast<uintptr_t>(a.out) & 15) == 0 && a.g.D2 < (1ll << 40) &&
+         (a.g.D2 + D1_TILE - 1) / D1_TILE < (1ll << 31) && a.q.twoeb < 1e300;
+}
+
+cudaError_t launch_decompress_1d(int B, const DecompressArgs& a, cudaStream_t st) {
+  switch (B) {
+    case 8: return run_d1d<8>(a, st);
+    case 16: return run_d1d<16>(a, st);
+    case 32: return run_d1d<32>(a, st);
+    case 64: return run_d1d<64>(a, st);
+    case 256: return run_d1d<256>(a, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace vlz

@@ -4,6 +4,7 @@
 namespace vlz {
 
 cudaError_t launch_compress_nd1(int B, int mode, const CompressArgs& a, cudaStream_t st) {
+  if (d1_fast_compress_ok(a)) return launch_compress_1d(B, mode, a, st);
   switch (B) {
     case 8: return run_compress_b<1, 8, 4>(mode, a, st);
     case 16: return run_compress_b<1, 16, 4>(mode, a, st);

@@ -89,6 +89,7 @@ static cudaError_t run_d(bool u32, const DecompressArgs& a, cudaStream_t st) {
 }
 
 cudaError_t launch_decompress(int nd, int B, bool u32, const DecompressArgs& a, cudaStream_t st) {
+  if (nd == 1 && d1_fast_decompress_ok(u32, a)) return launch_decompress_1d(B, a, st);
   if (nd == 1) {
     switch (B) {
       case 8: return run_d<1, 8, 4>(u32, a, st);

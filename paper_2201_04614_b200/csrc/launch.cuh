@@ -64,6 +64,11 @@ cudaError_t launch_compress_nd1(int B, int mode, const CompressArgs& a, cudaStre
 cudaError_t launch_compress_nd2(int B, int mode, const CompressArgs& a, cudaStream_t st);
 cudaError_t launch_compress_nd3(int B, int mode, const CompressArgs& a, cudaStream_t st);
 cudaError_t launch_decompress(int nd, int B, bool u32, const DecompressArgs& a, cudaStream_t st);
+// fused 1-D kernels (k_1d.cu) and when they apply
+bool d1_fast_compress_ok(const CompressArgs& a);
+bool d1_fast_decompress_ok(bool u32, const DecompressArgs& a);
+cudaError_t launch_compress_1d(int B, int mode, const CompressArgs& a, cudaStream_t st);
+cudaError_t launch_decompress_1d(int B, const DecompressArgs& a, cudaStream_t st);
 
 // window width (columns per warp tile) used for (nd, B)
 inline int vpl_for(int nd, int B, bool compress = false) {

@@ -255,3 +255,41 @@ def test_outlier_report_matches_reference():
                     total=r.total_outliers, border=r.border_outliers, reduction=red)
                for r, red in rows]
         assert got == c["rows"], c["tag"]
+
+
+@pytest.mark.parametrize("b", [8, 16, 32, 64, 256])
+def test_fused_1d_kernels(oracle, b):
+    # dq_1d.cuh: full 2048-element tiles through the bulk-copy ring plus a
+    # partial tail tile with a partial last block; random walk + spikes give
+    # outliers in most blocks, near-ties exercise the exact fp64 path
+    rng = np.random.default_rng(b)
+    n = 2048 * 37 + 3 * 256 + 13
+    walk = np.cumsum(rng.normal(0, 1, n)) * 0.01 + np.sin(np.arange(n) * (2 * np.pi / 4096))
+    data = walk.astype(np.float32)
+    data[rng.integers(0, n, 400)] *= 9.0
+    eb = float(np.float32(1e-4 * (data.max() - data.min())))
+    for pol in ("zero", "mean:global", "max:global", "min:block", "mean:block", "mean:edge",
+                "max:edge"):
+        s = _check_full(oracle, data, eb, b, pol, 512)
+        assert s.outlier_values.size > 0
+
+
+def test_fused_1d_int64_rows(oracle):
+    # |q| >= 2^30 in some rows: those rows go to the int64 generic kernels
+    # through the redo list (compress and decompress)
+    rng = np.random.default_rng(11)
+    data = (rng.uniform(-1, 1, 2048 * 9 + 100) * 2.0e9).astype(np.float32)
+    for b in (8, 64, 256):
+        for pol in ("zero", "mean:global", "max:block"):
+            _check_full(oracle, data, 0.9, b, pol, 32768)
+
+
+def test_fused_1d_kernels_many_tiles_per_warp(oracle):
+    # ~20 M elements: every warp of the persistent grid streams several tiles,
+    # so the bulk-copy ring is refilled and reused (stage / phase bookkeeping)
+    rng = np.random.default_rng(21)
+    n = 20 * 1024 * 1024 + 1000
+    data = (np.cumsum(rng.normal(0, 1, n)) * 0.01).astype(np.float32)
+    eb = float(np.float32(1e-4 * (data.max() - data.min())))
+    for b, pol in ((64, "mean:global"), (256, "zero"), (8, "max:block")):
+        _check_full(oracle, data, eb, b, pol, 512)
