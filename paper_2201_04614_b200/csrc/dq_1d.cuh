@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(D1_WARPS * 32, 4)
         unsigned cadd = 0x00010001u;  // common path: code = u + 1 per packed half
         int tot = 0;
         const unsigned orig_mask = lead ? 1u : 0u;
-        if (__any_sync(FULL, umax > span || (badm & ~orig_mask) != 0u || (lead && o_out))) {
+        if (__any_sync(FULL, umax > span || (badm & ~orig_mask) != 0u)) {
           unsigned om = 0;
 #pragma unroll
           for (int j = 0; j < VPL; ++j) {
@@ -263,15 +263,21 @@ __global__ void __launch_bounds__(D1_WARPS * 32, 4)
           for (int j = 0; j < VPL; ++j)
             if ((om >> j) & 1u) slot[k++] = v[j];
         } else if (lead) {
-          u[0] = ocode - 1u;  // ocode >= 1 here
+          u[0] = 0u;  // packed below without a carry; the origin code is patched in
         }
-        // ---- codes (element order is the canonical order in 1-D)
+        // ---- codes (element order is the canonical order in 1-D); the
+        // origin code (0 for an outlier origin) replaces the lead's low half
         if (nvalid == VPL) {
-          st_codes<VPL>(a.codes + el, u, cadd);
+          uint32_t w[VPL / 2];
+#pragma unroll
+          for (int k = 0; k < VPL / 2; ++k) w[k] = __byte_perm(u[2 * k], u[2 * k + 1], 0x5410) + cadd;
+          if (lead) w[0] = (w[0] & 0xffff0000u) | ocode;
+          *reinterpret_cast<uint4*>(a.codes + el) = make_uint4(w[0], w[1], w[2], w[3]);
         } else {
 #pragma unroll
           for (int j = 0; j < VPL; ++j)
-            if (j < nvalid) a.codes[el + j] = (uint16_t)(u[j] + (cadd & 1u));
+            if (j < nvalid)
+              a.codes[el + j] = (j == 0 && lead) ? (uint16_t)ocode : (uint16_t)(u[j] + (cadd & 1u));
         }
         // ---- block end (the block lies inside this row)
         if (lead && nvalid > 0) {
@@ -399,14 +405,18 @@ __global__ void __launch_bounds__(D1_WARPS * 32, 4)
 #pragma unroll
           for (int j = 0; j < VPL; ++j) c[j] = j < nvalid ? (unsigned)codes[el + j] : (unsigned)R;
         }
-        unsigned cmin = c[0], cmax = c[0];
+        // sentinels other than the block origins decide the path: an origin
+        // sentinel only re-bases its block (d = d_s + prefix of later deltas)
+        unsigned cmin = lead ? c[1] : c[0], cmax = c[0];
 #pragma unroll
         for (int j = 1; j < VPL; ++j) {
           cmin = c[j] < cmin ? c[j] : cmin;
           cmax = c[j] > cmax ? c[j] : cmax;
         }
+        if (!lead) cmin = c[0] < cmin ? c[0] : cmin;
         bool wide = (s064 >= (1ll << 30)) || (s064 <= -(1ll << 30));
         const int s0 = (int)s064;
+        int sb = s0;  // base of the block's prefix
         int h[VPL];
         int pvc = 0;
         unsigned smask = 0;
@@ -414,6 +424,20 @@ __global__ void __launch_bounds__(D1_WARPS * 32, 4)
         float vs[VPL];
         if (!__any_sync(FULL, cmin == 0u)) {
           // common path: prefix of delta across the block's lanes
+          if (lead && c[0] == 0u && bvalid) {  // origin sentinel
+            const long long off = a.offsets[bi];
+            const long long avail = imax64(0, imin64(cnt, a.n_outliers - off));
+            vs[0] = avail > 0 ? a.outliers[off] : 0.f;
+            bool qok;
+            const int nq = quant_fast(vs[0], a.q, qok);
+            const long long ds = qok ? (long long)nq : quant_value(vs[0], a.q.twoeb);
+            wide |= (ds >= (1ll << 30)) || (ds <= -(1ll << 30));
+            sb = (int)ds;
+            c[0] = (unsigned)R;  // delta 0: the base carries the origin
+            smask = 1u;
+            run = 1;
+          }
+          if (LPB > 1) sb = __shfl_sync(FULL, sb, lane & ~(LPB - 1));
           h[0] = (int)c[0] - R;
 #pragma unroll
           for (int j = 1; j < VPL; ++j) h[j] = h[j - 1] + ((int)c[j] - R);
@@ -477,7 +501,7 @@ __global__ void __launch_bounds__(D1_WARPS * 32, 4)
         int dmax = 0, dmin = 0;
 #pragma unroll
         for (int j = 0; j < VPL; ++j) {
-          const int dv = s0 + h[j] + pvc;
+          const int dv = sb + h[j] + pvc;
           dmax = max(dmax, dv);
           dmin = min(dmin, dv);
           const double dd = __dadd_rn(__hiloint2double(0x43300000, dv ^ (int)0x80000000),
