@@ -51,7 +51,21 @@ struct D1Args {
   DecompressArgs d;
   unsigned int* redo_count;
   long long* redo_list;
+  int meta_smem;  // decompress: per-block counts/offsets/scalars also streamed by the ring
 };
+
+// decompress ring stage: codes | counts | offsets | scalars of the tile's blocks
+template <int B>
+struct D1DStage {
+  static constexpr int MB = D1_TILE / B;  // blocks per tile
+  static constexpr int CODES = 0, COUNTS = D1_TILE * 2, OFFS = COUNTS + MB * 8,
+                       SCAL = OFFS + MB * 8;
+  static constexpr int BYTES = (SCAL + MB * 8 + 127) / 128 * 128;
+};
+template <int B>
+__host__ __device__ constexpr int d1d_warp_smem() {
+  return D1_STAGES * D1DStage<B>::BYTES + 128;
+}
 
 template <int ELEM_BYTES>
 __host__ __device__ constexpr int d1_warp_smem() {
@@ -352,7 +366,8 @@ __global__ void __launch_bounds__(D1_WARPS * 32, 4)
     dq_decompress_1d_kernel(const __grid_constant__ D1Args fa) {
   constexpr int VPL = D1_VPL;
   constexpr int LPB = B / VPL;
-  constexpr int WS = d1_warp_smem<2>();
+  using DS = D1DStage<B>;
+  constexpr int WS = d1d_warp_smem<B>();
   extern __shared__ __align__(128) unsigned char smem_d1d[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -363,8 +378,26 @@ __global__ void __launch_bounds__(D1_WARPS * 32, 4)
   const int64_t ntiles = (N + D1_TILE - 1) / D1_TILE;
   const int64_t nfull = N / D1_TILE;
   D1Ring rg{smem_d1d + (size_t)wib * WS,
-            reinterpret_cast<uint64_t*>(smem_d1d + (size_t)wib * WS + D1_STAGES * D1_TILE * 2), 0,
+            reinterpret_cast<uint64_t*>(smem_d1d + (size_t)wib * WS + D1_STAGES * DS::BYTES), 0,
             0u};
+  const bool meta = fa.meta_smem != 0;
+  const bool scal_blocks = a.mode == MODE_BLOCK || a.mode == MODE_EDGE;
+  // one stage: the tile's codes and, with `meta`, its blocks' counts /
+  // offsets (/ scalars) -- one mbarrier transaction
+  auto issue = [&](uint32_t t, int slot) {
+    if ((int64_t)t < nfull && lane == 0) {
+      unsigned char* dst = rg.ring + slot * DS::BYTES;
+      const uint32_t bytes = D1_TILE * 2 + (meta ? DS::MB * 8 * (scal_blocks ? 3 : 2) : 0);
+      mbar_arrive_expect_tx(&rg.bars[slot], bytes);
+      bulk_g2s(dst + DS::CODES, codes + (int64_t)t * D1_TILE, D1_TILE * 2, &rg.bars[slot]);
+      if (meta) {
+        const int64_t b0 = (int64_t)t * DS::MB;
+        bulk_g2s(dst + DS::COUNTS, a.counts + b0, DS::MB * 8, &rg.bars[slot]);
+        bulk_g2s(dst + DS::OFFS, a.offsets + b0, DS::MB * 8, &rg.bars[slot]);
+        if (scal_blocks) bulk_g2s(dst + DS::SCAL, a.scalars + b0, DS::MB * 8, &rg.bars[slot]);
+      }
+    }
+  };
   if (lane == 0) {
     for (int s = 0; s < D1_STAGES; ++s) mbar_init(&rg.bars[s], 1);
     fence_mbar_init();
@@ -372,16 +405,21 @@ __global__ void __launch_bounds__(D1_WARPS * 32, 4)
   __syncwarp();
   const uint32_t nwarps = gridDim.x * D1_WARPS;
   const uint32_t first = blockIdx.x * D1_WARPS + wib;
-  for (int s = 0; s < D1_STAGES; ++s) rg.issue<2>(codes, first + s * nwarps, nfull, s, lane);
+  for (int s = 0; s < D1_STAGES; ++s) issue(first + s * nwarps, s);
 
   const int xin = (lane * VPL) % B;
   const int gl = lane & (LPB - 1);
   const bool lead = xin == 0;
   long long sent_acc = 0;
+  const long long s0g = a.mode == MODE_GLOBAL ? a.scalars[0] : 0;
 
   for (uint32_t tile = first; (int64_t)tile < ntiles; tile += nwarps) {
     const bool full = (int64_t)tile < nfull;
-    const uint16_t* sm = reinterpret_cast<const uint16_t*>(rg.ring + rg.stage * D1_TILE * 2);
+    const unsigned char* stg = rg.ring + rg.stage * DS::BYTES;
+    const uint16_t* sm = reinterpret_cast<const uint16_t*>(stg + DS::CODES);
+    const long long* smc = reinterpret_cast<const long long*>(stg + DS::COUNTS);
+    const long long* smo = reinterpret_cast<const long long*>(stg + DS::OFFS);
+    const long long* sms = reinterpret_cast<const long long*>(stg + DS::SCAL);
     if (full) mbar_wait(&rg.bars[rg.stage], rg.parity);
     auto row = [&](auto full_tag, int r, int64_t e0) {
         constexpr bool WHOLE = decltype(full_tag)::value;  // (FULL is the warp mask)
@@ -389,13 +427,16 @@ __global__ void __launch_bounds__(D1_WARPS * 32, 4)
         const int nvalid = WHOLE ? VPL : (int)imax64(0, imin64(VPL, N - el));
         const int64_t bi = el / B;
         const bool bvalid = nvalid > 0;
-        // block metadata (every lane of a block reads the same words)
-        long long s064 = 0, cnt = 0;
+        // block metadata (every lane of a block reads the same words): from
+        // the stage when the ring streams it, else from global memory
+        const int lb = (r * D1_ROW + lane * VPL) / B;  // block within the tile
+        const bool msm = WHOLE && meta;
+        long long s064 = s0g, cnt = 0;
         if (bvalid) {
-          if (a.mode == MODE_GLOBAL) s064 = a.scalars[0];
-          else if (a.mode == MODE_BLOCK || a.mode == MODE_EDGE) s064 = a.scalars[bi];
-          cnt = a.counts[bi];
+          if (scal_blocks) s064 = msm ? sms[lb] : a.scalars[bi];
+          cnt = msm ? smc[lb] : a.counts[bi];
         }
+        auto offset_of = [&]() -> long long { return msm ? smo[lb] : a.offsets[bi]; };
         unsigned c[VPL];
         if (WHOLE) {
           const uint4 pk = *reinterpret_cast<const uint4*>(sm + r * D1_ROW + lane * VPL);
@@ -425,7 +466,7 @@ __global__ void __launch_bounds__(D1_WARPS * 32, 4)
         if (!__any_sync(FULL, cmin == 0u)) {
           // common path: prefix of delta across the block's lanes
           if (lead && c[0] == 0u && bvalid) {  // origin sentinel
-            const long long off = a.offsets[bi];
+            const long long off = offset_of();
             const long long avail = imax64(0, imin64(cnt, a.n_outliers - off));
             vs[0] = avail > 0 ? a.outliers[off] : 0.f;
             bool qok;
@@ -455,7 +496,7 @@ __global__ void __launch_bounds__(D1_WARPS * 32, 4)
           const int excl = group_excl_scan<LPB>(__popc(smask), lane, run);
           long long off = 0, avail = 0;
           if (smask) {
-            off = a.offsets[bi];
+            off = offset_of();
             avail = imax64(0, imin64(cnt, a.n_outliers - off));
           }
           int k = excl;
@@ -532,7 +573,7 @@ __global__ void __launch_bounds__(D1_WARPS * 32, 4)
         if (lead && bvalid) {
           sent_acc += run;
           // (a block with no stored and no found outliers needs no offset)
-          const long long off = (cnt != 0 || run != 0) ? a.offsets[bi] : 0;
+          const long long off = (cnt != 0 || run != 0) ? offset_of() : 0;
           const long long avail = imax64(0, imin64(cnt, a.n_outliers - off));
           int st = 0;
           if (bad_any) st = 4;
@@ -555,7 +596,7 @@ __global__ void __launch_bounds__(D1_WARPS * 32, 4)
     }
     __syncwarp();
     fence_proxy_async_smem();
-    rg.issue<2>(codes, tile + D1_STAGES * nwarps, nfull, rg.stage, lane);
+    issue(tile + D1_STAGES * nwarps, rg.stage);
     if (++rg.stage == D1_STAGES) {
       rg.stage = 0;
       rg.parity ^= 1u;

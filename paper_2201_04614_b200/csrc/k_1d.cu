@@ -89,8 +89,13 @@ static cudaError_t run_d1d(const DecompressArgs& a, cudaStream_t st) {
   fa.d = a;
   fa.redo_count = const_cast<unsigned int*>(a.redo_count);
   fa.redo_list = const_cast<long long*>(a.redo_list);
+  // the ring also streams counts / offsets / block scalars when aligned
+  const bool scal = a.mode == MODE_BLOCK || a.mode == MODE_EDGE;
+  fa.meta_smem = ((reinterpret_cast<uintptr_t>(a.counts) & 15) == 0) &&
+                 ((reinterpret_cast<uintptr_t>(a.offsets) & 15) == 0) &&
+                 (!scal || (reinterpret_cast<uintptr_t>(a.scalars) & 15) == 0);
   auto kern = dq_decompress_1d_kernel<B>;
-  constexpr int smem = D1_WARPS * d1_warp_smem<2>();
+  constexpr int smem = D1_WARPS * d1d_warp_smem<B>();
   int64_t grid = 0;
   cudaError_t e = d1_grid(kern, smem, (a.g.D2 + D1_TILE - 1) / D1_TILE, grid);
   if (e != cudaSuccess) return e;
