@@ -361,8 +361,12 @@ __global__ void __launch_bounds__(D1_WARPS * 32, 4)
 }
 
 // -------------------------------------------------------------- decompress
+#ifndef VLZ_D1D_MINB
+#define VLZ_D1D_MINB 5  // CTAs per SM the 1-D decompress register budget targets
+                        // (4: 116 regs, 0.44 ms at 1-D 256M b=256; 5: 0.41 ms; 6: 0.51 ms)
+#endif
 template <int B>
-__global__ void __launch_bounds__(D1_WARPS * 32, 4)
+__global__ void __launch_bounds__(D1_WARPS * 32, VLZ_D1D_MINB)
     dq_decompress_1d_kernel(const __grid_constant__ D1Args fa) {
   constexpr int VPL = D1_VPL;
   constexpr int LPB = B / VPL;
