@@ -150,8 +150,12 @@ __device__ __forceinline__ bool compress_tile(const CompressArgs& a, int64_t til
       unsigned badm = 0;
 #pragma unroll
       for (int j = 0; j < VPL; ++j) {
-        bool bad, ovf;
-        n[j] = quant_exact(v[j], a.q, bad, ovf);
+        // exact-fast float32 quotient first (DESIGN.md proof: when it reports
+        // ok the rounding and the narrowing check are already decided), fp64
+        // only for the undecided elements
+        bool bad = false, ovf = false, fok;
+        n[j] = quant_fast(v[j], a.q, fok);
+        if (!fok) n[j] = quant_exact(v[j], a.q, bad, ovf);
         if (j < nvalid) {
           if (bad) badm |= 1u << j;
           if (ovf) {
