@@ -88,7 +88,7 @@ struct FastShape {
   static constexpr int PLANE_FLOATS = S::BY * S::W;
   static constexpr int PLANE_BYTES = PLANE_FLOATS * 4;
   // a plane streams in SPLIT ring stages of STAGE_ROWS rows each
-  static constexpr int SPLIT = 1;
+  static constexpr int SPLIT = S::BY >= 32 ? S::BY / 8 : 1;  // b >= 32: 8-row stages
   static constexpr int STAGE_ROWS = S::BY / SPLIT;
   static constexpr int STAGE_FLOATS = STAGE_ROWS * S::W;
   static constexpr int STAGE_BYTES = STAGE_FLOATS * 4;
@@ -265,7 +265,7 @@ __device__ __forceinline__ void fast_tile(const FastArgs& fa, uint32_t tile, con
     int prow[VPL];
 #pragma unroll
     for (int j = 0; j < VPL; ++j) prow[j] = 0;  // Dy zero fill at the block's first row
-    int psum = 0;  // |sum of a plane| < BY * W / 32 * VPL * 2^24 < 2^31
+    int psum = 0;  // |sum of a stage| < STAGE_ROWS * VPL * 2^24 < 2^31 (flushed per stage)
     for (int part = 0; part < F::SPLIT; ++part) {
     const float* plane = ring + cons.stage * F::STAGE_FLOATS + lane * VPL;
     unsigned char* const stage_bytes = reinterpret_cast<unsigned char*>(ring + cons.stage * F::STAGE_FLOATS);
@@ -463,11 +463,12 @@ __device__ __forceinline__ void fast_tile(const FastArgs& fa, uint32_t tile, con
     fence_proxy_async_smem();
     prod.issue(g, &fa.tmap, ring, bars, lane, nwarps);
     cons.advance();
-    }
-    if (MODE == MODE_GLOBAL) {
+    if (MODE == MODE_GLOBAL && K == 3) {  // per stage: |psum| < STAGE_ROWS * VPL * 2^24
       tacc.sum += psum;
-      tcnt += (long long)nvalid * ey;
+      psum = 0;
     }
+    }
+    if (MODE == MODE_GLOBAL) tcnt += (long long)nvalid * ey;
   }
 
   // int32 stencil may have wrapped: hand the whole tile to the int64 redo

@@ -25,7 +25,7 @@ static bool make_code_map(CUtensorMap* m, const void* codes, int64_t nblocks) {
 
 template <int ND, int B>
 constexpr bool has_dfast() {
-  return (ND == 3 || ND == 2) && (B == 8 || B == 16);
+  return (ND == 3 || ND == 2) && (B == 8 || B == 16 || B == 32);
 }
 
 template <int ND, int B, int VPL>
@@ -109,7 +109,7 @@ cudaError_t launch_decompress(int nd, int B, bool u32, const DecompressArgs& a, 
     switch (B) {
       case 8: return run_d<3, 8, VLZ_VPL_3D8>(u32, a, st);
       case 16: return run_d<3, 16, VLZ_DVPL_3D16>(u32, a, st);
-      case 32: return run_d<3, 32, 4>(u32, a, st);
+      case 32: return run_d<3, 32, 2>(u32, a, st);
       case 64: return run_d<3, 64, 2>(u32, a, st);
     }
   }

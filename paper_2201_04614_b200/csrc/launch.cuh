@@ -75,6 +75,7 @@ inline int vpl_for(int nd, int B, bool compress = false) {
   if (compress && nd == 3 && B == 8) return VLZ_VPL_C3D8;
   if (nd == 1 && B == 256) return 8;
   if (nd == 3 && B == 64) return 2;
+  if (nd == 3 && B == 32) return 2;
   if (nd == 3 && B == 16) return compress ? VLZ_CVPL_3D16 : VLZ_DVPL_3D16;
   if (nd == 3 && B == 8) return VLZ_VPL_3D8;
   return 4;

@@ -47,7 +47,7 @@ inline bool make_plane_map(CUtensorMap* m, const float* in, const Geo& g, int W,
 
 template <int ND, int B>
 constexpr bool has_fast() {
-  return (ND == 3 || ND == 2) && (B == 8 || B == 16);
+  return (ND == 3 || ND == 2) && (B == 8 || B == 16 || B == 32 || B == 64);
 }
 
 template <int ND, int B, int VPL, int MODE, int K>

@@ -293,3 +293,20 @@ def test_fused_1d_kernels_many_tiles_per_warp(oracle):
     eb = float(np.float32(1e-4 * (data.max() - data.min())))
     for b, pol in ((64, "mean:global"), (256, "zero"), (8, "max:block")):
         _check_full(oracle, data, eb, b, pol, 512)
+
+
+@pytest.mark.parametrize("shape,b", [((70, 96, 200), 32), ((64, 64, 128), 32),
+                                     ((130, 140, 136), 64), ((300, 520), 32),
+                                     ((260, 600), 64), ((256, 512), 64)])
+def test_fast_kernels_large_blocks(oracle, shape, b):
+    # b = 32 / 64 through the fused kernels (8-row ring stages): interior
+    # tiles and partial windows / block rows, outliers and every policy family
+    rng = np.random.default_rng(sum(shape) * b)
+    idx = np.indices(shape).astype(np.float64)
+    smooth = sum(np.sin(0.05 * (k + 1) * idx[k]) * 30.0 for k in range(len(shape)))
+    data = (smooth + rng.normal(0, 0.05, shape)).astype(np.float32)
+    data.ravel()[rng.integers(0, data.size, 200)] *= 6.0
+    for eb, pol in ((1e-3, "mean:global"), (1e-4, "zero"), (1e-3, "max:block"),
+                    (1e-3, "mean:edge"), (1e-3, "min:global")):
+        s = _check_full(oracle, data, eb, b, pol, 512)
+        assert s.outlier_values.size > 0
