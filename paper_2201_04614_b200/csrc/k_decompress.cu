@@ -25,7 +25,7 @@ static bool make_code_map(CUtensorMap* m, const void* codes, int64_t nblocks) {
 
 template <int ND, int B>
 constexpr bool has_dfast() {
-  return (ND == 3 || ND == 2) && (B == 8 || B == 16 || B == 32);
+  return (ND == 3 || ND == 2) && (B == 8 || B == 16 || B == 32 || B == 64);
 }
 
 template <int ND, int B, int VPL>
