@@ -106,6 +106,7 @@ __device__ __forceinline__ void d1_redo_row(unsigned int* count, long long* list
 template <int B, int MODE, int K>
 __global__ void __launch_bounds__(D1_WARPS * 32, 4)
     dq_compress_1d_kernel(const __grid_constant__ D1Args fa) {
+  pdl_enter();
   constexpr int VPL = D1_VPL;
   constexpr int LPB = B / VPL;  // lanes per block: 1 ... 32
   constexpr unsigned MAGIC_BITS = 0x4B400000u;
@@ -368,6 +369,7 @@ __global__ void __launch_bounds__(D1_WARPS * 32, 4)
 template <int B>
 __global__ void __launch_bounds__(D1_WARPS * 32, VLZ_D1D_MINB)
     dq_decompress_1d_kernel(const __grid_constant__ D1Args fa) {
+  pdl_enter();
   constexpr int VPL = D1_VPL;
   constexpr int LPB = B / VPL;
   using DS = D1DStage<B>;

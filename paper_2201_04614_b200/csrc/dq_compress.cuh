@@ -354,6 +354,7 @@ __device__ __forceinline__ bool compress_tile(const CompressArgs& a, int64_t til
 //               directly in int64 (dq_compress_fast.cuh).
 template <int ND, int B, int VPL, int MODE, bool LIST = false>
 __global__ void __launch_bounds__(128) dq_compress_kernel(CompressArgs a) {
+  pdl_enter();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int PB = plane_smem_bytes<ND, B, VPL>();
   const int lane = threadIdx.x & 31;

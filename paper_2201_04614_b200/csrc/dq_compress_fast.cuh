@@ -528,6 +528,7 @@ __device__ __forceinline__ void fast_tile(const FastArgs& fa, uint32_t tile, con
 template <int ND, int B, int VPL, int MODE, int K>
 __global__ void __launch_bounds__(FAST_WARPS * 32, (FastShape<ND, B, VPL>::MINB))
     dq_compress_fast_kernel(const __grid_constant__ FastArgs fa) {
+  pdl_enter();
   using S = Shape<ND, B, VPL>;
   using F = FastShape<ND, B, VPL>;
   extern __shared__ __align__(128) unsigned char smem_fast[];

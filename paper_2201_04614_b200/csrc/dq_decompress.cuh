@@ -256,6 +256,7 @@ __device__ __forceinline__ void decompress_tile(const DecompressArgs& a, int64_t
 // and tiles that failed the int32 exactness check), in int64 as always.
 template <int ND, int B, int VPL, typename CT, bool LIST = false>
 __global__ void __launch_bounds__(128) dq_decompress_kernel(DecompressArgs a) {
+  pdl_enter();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int PB = plane_smem_bytes<ND, B, VPL>();
   const int lane = threadIdx.x & 31;

@@ -447,6 +447,7 @@ __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, c
 template <int ND, int B, int VPL, bool EDGES>
 __global__ void __launch_bounds__(FAST_WARPS * 32, (EDGES && B == 8) ? 3 : 4)
     dq_decompress_fast_kernel(const __grid_constant__ DFastArgs fa) {
+  pdl_enter();
   using F = DFastShape<ND, B, VPL>;
   extern __shared__ __align__(128) unsigned char smem_dfast[];
   const int lane = threadIdx.x & 31;
@@ -494,6 +495,7 @@ __host__ __device__ constexpr int dtma_smem_bytes() {
 template <int ND, int B, int VPL, bool EDGES>
 __global__ void __launch_bounds__(FAST_WARPS * 32, EDGES ? 3 : VLZ_DTMA_MINB)
     dq_decompress_tma_kernel(const __grid_constant__ DFastArgs fa) {
+  pdl_enter();
   using T = DTmaShape<ND, B, VPL, EDGES>;
   extern __shared__ __align__(1024) unsigned char smem_dtma[];
   // align by an offset from the shared array itself (keeps the accesses LDS/STS)

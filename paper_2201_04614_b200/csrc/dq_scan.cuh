@@ -189,6 +189,7 @@ __device__ __forceinline__ T cta_excl_scan(T v, T* s_warp, T& total) {
 // a non-global origin sits in slot 0).
 template <int SCAN_IPT>
 __global__ void __launch_bounds__(SCAN_THREADS) dq_scan_kernel(ScanArgs a) {
+  pdl_enter();
   constexpr int SCAN_CH = SCAN_THREADS * SCAN_IPT;
   constexpr int HEAVY = 32;  // blocks with >= HEAVY scratch outliers: whole-warp copy
   // padded so that both the coalesced ([k][tid]) and the per-thread
@@ -415,6 +416,7 @@ inline int64_t offsets_chunks(int64_t nblocks) {
 }
 
 __global__ void __launch_bounds__(SCAN_THREADS) dq_offsets_kernel(ScanArgs a, int64_t span) {
+  pdl_enter();
   __shared__ long long s_val[OFF_SWEEP + SCAN_THREADS];  // padded (pad_l)
   __shared__ long long s_warp[SCAN_THREADS / 32];
   __shared__ int s_first[SCAN_THREADS / 32];

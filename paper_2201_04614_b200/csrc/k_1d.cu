@@ -32,7 +32,8 @@ static cudaError_t run_c1d(const CompressArgs& a, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   const bool t = g_timing.load(std::memory_order_relaxed);
   if (t) timing_mark(TK_COMPRESS, true, st);
-  kern<<<(unsigned)grid, D1_WARPS * 32, smem, st>>>(fa);
+  e = launch_k(kern, (unsigned)grid, D1_WARPS * 32, smem, st, fa);
+  if (e != cudaSuccess) return e;
   if (t) timing_mark(TK_COMPRESS, false, st);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   e = cudaGetLastError();
@@ -42,7 +43,8 @@ static cudaError_t run_c1d(const CompressArgs& a, cudaStream_t st) {
   auto redo = dq_compress_kernel<1, B, VG, MODE, true>;
   constexpr int psmem = 4 * plane_smem_bytes<1, B, VG>();
   if (t) timing_mark(TK_REDO, true, st);
-  redo<<<(unsigned)num_sms(), 128, psmem, st>>>(a);
+  e = launch_k(redo, (unsigned)num_sms(), 128, psmem, st, a);
+  if (e != cudaSuccess) return e;
   if (t) timing_mark(TK_REDO, false, st);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
@@ -66,8 +68,12 @@ static cudaError_t run_c1d_b(int mode, const CompressArgs& a, cudaStream_t st) {
   }
 }
 
+// below ~4 M elements the call is launch bound: one generic kernel beats the
+// fused kernel + its (usually empty) int64 redo launch
+constexpr int64_t D1_MIN_N = 1ll << 22;
+
 bool d1_fast_compress_ok(const CompressArgs& a) {
-  return a.redo_list != nullptr && (reinterpret_cast<uintptr_t>(a.in) & 15) == 0 &&
+  return a.g.D2 >= D1_MIN_N && a.redo_list != nullptr && (reinterpret_cast<uintptr_t>(a.in) & 15) == 0 &&
          (reinterpret_cast<uintptr_t>(a.codes) & 15) == 0 && a.g.D2 < (1ll << 40) &&
          (a.g.D2 + D1_TILE - 1) / D1_TILE < (1ll << 31);
 }
@@ -101,7 +107,8 @@ static cudaError_t run_d1d(const DecompressArgs& a, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   const bool t = g_timing.load(std::memory_order_relaxed);
   if (t) timing_mark(TK_DECOMPRESS, true, st);
-  kern<<<(unsigned)grid, D1_WARPS * 32, smem, st>>>(fa);
+  e = launch_k(kern, (unsigned)grid, D1_WARPS * 32, smem, st, fa);
+  if (e != cudaSuccess) return e;
   if (t) timing_mark(TK_DECOMPRESS, false, st);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   e = cudaGetLastError();
@@ -111,14 +118,15 @@ static cudaError_t run_d1d(const DecompressArgs& a, cudaStream_t st) {
   auto redo = dq_decompress_kernel<1, B, VG, uint16_t, true>;
   constexpr int psmem = 4 * plane_smem_bytes<1, B, VG>();
   if (t) timing_mark(TK_REDO, true, st);
-  redo<<<(unsigned)num_sms() * 2, 128, psmem, st>>>(a);
+  e = launch_k(redo, (unsigned)num_sms() * 2, 128, psmem, st, a);
+  if (e != cudaSuccess) return e;
   if (t) timing_mark(TK_REDO, false, st);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
 
 bool d1_fast_decompress_ok(bool u32, const DecompressArgs& a) {
-  return !u32 && a.redo_list != nullptr && (reinterpret_cast<uintptr_t>(a.codes) & 15) == 0 &&
+  return a.g.D2 >= D1_MIN_N && !u32 && a.redo_list != nullptr && (reinterpret_cast<uintptr_t>(a.codes) & 15) == 0 &&
          (reinterpret_cast<uintptr_t>(a.out) & 15) == 0 && a.g.D2 < (1ll << 40) &&
          (a.g.D2 + D1_TILE - 1) / D1_TILE < (1ll << 31) && a.q.twoeb < 1e300;
 }

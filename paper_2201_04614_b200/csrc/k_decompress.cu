@@ -67,7 +67,8 @@ static cudaError_t run_d(bool u32, const DecompressArgs& a, cudaStream_t st) {
       if (grid < 1) grid = 1;
       const bool t = g_timing.load(std::memory_order_relaxed);
       if (t) timing_mark(TK_DECOMPRESS, true, st);
-      kern<<<(unsigned)grid, FAST_WARPS * 32, fsmem, st>>>(fa);
+      e = launch_k(kern, (unsigned)grid, FAST_WARPS * 32, fsmem, st, fa);
+      if (e != cudaSuccess) return e;
       if (t) timing_mark(TK_DECOMPRESS, false, st);
       g_launches.fetch_add(1, std::memory_order_relaxed);
       e = cudaGetLastError();
@@ -78,7 +79,8 @@ static cudaError_t run_d(bool u32, const DecompressArgs& a, cudaStream_t st) {
         if (e != cudaSuccess) return e;
       }
       if (t) timing_mark(TK_REDO, true, st);
-      redo<<<(unsigned)num_sms() * 2, 128, smem, st>>>(a);
+      e = launch_k(redo, (unsigned)num_sms() * 2, 128, smem, st, a);
+      if (e != cudaSuccess) return e;
       if (t) timing_mark(TK_REDO, false, st);
       g_launches.fetch_add(1, std::memory_order_relaxed);
       return cudaGetLastError();

@@ -29,6 +29,25 @@ extern std::atomic<long long> g_launches;
 
 int num_sms();
 
+// launch with the programmatic-stream-serialization attribute (PDL; the
+// kernels call pdl_enter() first).  VLZ_PDL=0 in the environment disables it.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem,
+                            cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 // optional per-kernel CUDA-event timing (vlz_timing / vlz_timing_collect)
 enum TimedKind { TK_INIT = 0, TK_COMPRESS = 1, TK_SCAN_C = 2, TK_SCAN_D = 3, TK_DECOMPRESS = 4,
                  TK_MINMAX = 5, TK_REDO = 6, TK_EDGE = 7, TK_COUNT = 8 };
@@ -53,10 +72,10 @@ inline cudaError_t launch_tiles(Kern kernel, int64_t ntiles, int smem, cudaStrea
   if (grid < 1) grid = 1;
   const int kind = std::is_same<Arg, CompressArgs>::value ? TK_COMPRESS : TK_DECOMPRESS;
   if (g_timing.load(std::memory_order_relaxed)) timing_mark(kind, true, st);
-  kernel<<<(unsigned)grid, 128, smem, st>>>(arg);
+  cudaError_t le = launch_k(kernel, (unsigned)grid, 128, smem, st, arg);
   if (g_timing.load(std::memory_order_relaxed)) timing_mark(kind, false, st);
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  return cudaGetLastError();
+  return le != cudaSuccess ? le : cudaGetLastError();
 }
 
 // per-(nd) dispatch entry points, one translation unit each

@@ -76,7 +76,8 @@ cudaError_t run_compress_shape(const CompressArgs& a, cudaStream_t st) {
       fa.redo_list = const_cast<long long*>(a.redo_list);
       const bool t = g_timing.load(std::memory_order_relaxed);
       if (t) timing_mark(TK_COMPRESS, true, st);
-      kern<<<(unsigned)grid, FAST_WARPS * 32, fsmem, st>>>(fa);
+      e = launch_k(kern, (unsigned)grid, FAST_WARPS * 32, fsmem, st, fa);
+      if (e != cudaSuccess) return e;
       if (t) timing_mark(TK_COMPRESS, false, st);
       g_launches.fetch_add(1, std::memory_order_relaxed);
       e = cudaGetLastError();
@@ -88,7 +89,8 @@ cudaError_t run_compress_shape(const CompressArgs& a, cudaStream_t st) {
         if (e != cudaSuccess) return e;
       }
       if (t) timing_mark(TK_REDO, true, st);
-      redo<<<(unsigned)num_sms(), 128, smem, st>>>(a);
+      e = launch_k(redo, (unsigned)num_sms(), 128, smem, st, a);
+      if (e != cudaSuccess) return e;
       if (t) timing_mark(TK_REDO, false, st);
       g_launches.fetch_add(1, std::memory_order_relaxed);
       return cudaGetLastError();

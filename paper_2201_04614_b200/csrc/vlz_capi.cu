@@ -10,6 +10,7 @@
 
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -54,6 +55,14 @@ void timing_mark(int kind, bool start, cudaStream_t st) {
   } else {
     g_trecs.push_back({kind, g_open[kind], e});
   }
+}
+
+bool pdl_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("VLZ_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return v;
 }
 
 int num_sms() {
@@ -160,6 +169,7 @@ WS carve(const Geo& g, void* base) {
 // one tiny kernel resets the result block, the counters and look-back words
 __global__ void init_kernel(vlz_result* res, unsigned int* ticket, unsigned int* done,
                             long long* stats, unsigned long long* lb, int64_t nchunks) {
+  pdl_enter();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i == 0) {
     if (res) {
@@ -193,7 +203,8 @@ cudaError_t launch_init(vlz_result* res, const WS& w, long long* stats, int64_t 
   if (blocks > 1024) blocks = 1024;
   const bool t = g_timing.load(std::memory_order_relaxed);
   if (t) timing_mark(TK_INIT, true, st);
-  init_kernel<<<(unsigned)blocks, 256, 0, st>>>(res, w.ticket, w.done, stats, w.lb, nchunks);
+  cudaError_t le = launch_k(init_kernel, (unsigned)blocks, 256, 0, st, res, w.ticket, w.done, stats, w.lb, nchunks);
+  if (le != cudaSuccess) return le;
   if (t) timing_mark(TK_INIT, false, st);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
@@ -202,22 +213,23 @@ cudaError_t launch_init(vlz_result* res, const WS& w, long long* stats, int64_t 
 cudaError_t launch_scan(const ScanArgs& a, cudaStream_t st) {
   const bool t = g_timing.load(std::memory_order_relaxed);
   const int kind = a.gather ? TK_SCAN_C : TK_SCAN_D;
+  cudaError_t le = cudaSuccess;
   if (t) timing_mark(kind, true, st);
   if (a.gather) {
     const unsigned nchunks = (unsigned)scan_chunks(a.g.nblocks);
     switch (scan_ipt(a.g.nblocks)) {
-      case 1: dq_scan_kernel<1><<<nchunks, SCAN_THREADS, 0, st>>>(a); break;
-      case 2: dq_scan_kernel<2><<<nchunks, SCAN_THREADS, 0, st>>>(a); break;
-      case 4: dq_scan_kernel<4><<<nchunks, SCAN_THREADS, 0, st>>>(a); break;
-      default: dq_scan_kernel<8><<<nchunks, SCAN_THREADS, 0, st>>>(a); break;
+      case 1: le = launch_k(dq_scan_kernel<1>, nchunks, SCAN_THREADS, 0, st, a); break;
+      case 2: le = launch_k(dq_scan_kernel<2>, nchunks, SCAN_THREADS, 0, st, a); break;
+      case 4: le = launch_k(dq_scan_kernel<4>, nchunks, SCAN_THREADS, 0, st, a); break;
+      default: le = launch_k(dq_scan_kernel<8>, nchunks, SCAN_THREADS, 0, st, a); break;
     }
   } else {
     const unsigned nchunks = (unsigned)offsets_chunks(a.g.nblocks);
-    dq_offsets_kernel<<<nchunks, SCAN_THREADS, 0, st>>>(a, offsets_span(a.g.nblocks));
+    le = launch_k(dq_offsets_kernel, nchunks, SCAN_THREADS, 0, st, a, offsets_span(a.g.nblocks));
   }
   if (t) timing_mark(kind, false, st);
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  return cudaGetLastError();
+  return le != cudaSuccess ? le : cudaGetLastError();
 }
 
 int to_rc(cudaError_t e) {

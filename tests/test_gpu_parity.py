@@ -259,11 +259,11 @@ def test_outlier_report_matches_reference():
 
 @pytest.mark.parametrize("b", [8, 16, 32, 64, 256])
 def test_fused_1d_kernels(oracle, b):
-    # dq_1d.cuh: full 2048-element tiles through the bulk-copy ring plus a
+    # dq_1d.cuh: full tiles through the bulk-copy ring plus a
     # partial tail tile with a partial last block; random walk + spikes give
     # outliers in most blocks, near-ties exercise the exact fp64 path
     rng = np.random.default_rng(b)
-    n = 2048 * 37 + 3 * 256 + 13
+    n = (1 << 22) + 2048 * 37 + 3 * 256 + 13  # >= 4 M: the fused path (k_1d.cu D1_MIN_N)
     walk = np.cumsum(rng.normal(0, 1, n)) * 0.01 + np.sin(np.arange(n) * (2 * np.pi / 4096))
     data = walk.astype(np.float32)
     data[rng.integers(0, n, 400)] *= 9.0
@@ -278,7 +278,7 @@ def test_fused_1d_int64_rows(oracle):
     # |q| >= 2^30 in some rows: those rows go to the int64 generic kernels
     # through the redo list (compress and decompress)
     rng = np.random.default_rng(11)
-    data = (rng.uniform(-1, 1, 2048 * 9 + 100) * 2.0e9).astype(np.float32)
+    data = (rng.uniform(-1, 1, (1 << 22) + 2048 * 9 + 100) * 2.0e9).astype(np.float32)
     for b in (8, 64, 256):
         for pol in ("zero", "mean:global", "max:block"):
             _check_full(oracle, data, 0.9, b, pol, 32768)
