@@ -136,6 +136,17 @@ int vlz_dq_decompress(const uint16_t* d_codes, const float* d_outliers,
                       int64_t n_outliers, const int64_t* d_counts, const int64_t* d_scalars,
                       const vlz_geom* g, const vlz_params* p, float* d_out,
                       vlz_result* d_result, void* d_ws, size_t ws_bytes, void* stream);
+/* As vlz_dq_decompress, with the stored outlier count read from device
+ * memory (e.g. &d_result->n_outliers of the vlz_dq_compress that produced the
+ * stream): a compress -> decompress round trip on one stream then needs no
+ * host synchronisation in between.  Replaces the host-side
+ * len(CodeStream.outlier_values) of reconstruct.py:87-91.  d_n_outliers must not
+ * alias d_result (the decompressor resets its own result block first). */
+int vlz_dq_decompress_dn(const uint16_t* d_codes, const float* d_outliers,
+                         const int64_t* d_n_outliers, const int64_t* d_counts,
+                         const int64_t* d_scalars, const vlz_geom* g, const vlz_params* p,
+                         float* d_out, vlz_result* d_result, void* d_ws, size_t ws_bytes,
+                         void* stream);
 int vlz_dq_decompress_u32(const uint32_t* d_codes, const float* d_outliers,
                           int64_t n_outliers, const int64_t* d_counts,
                           const int64_t* d_scalars, const vlz_geom* g, const vlz_params* p,

@@ -57,6 +57,8 @@ PROTOTYPES = {
                                          _vp, ctypes.c_size_t, _vp]),
     "vlz_dq_decompress_u32": (ctypes.c_int, [_vp, _vp, _i64, _vp, _vp, _P(Geom), _P(Params), _vp,
                                              _vp, _vp, ctypes.c_size_t, _vp]),
+    "vlz_dq_decompress_dn": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _P(Geom), _P(Params), _vp,
+                                            _vp, _vp, ctypes.c_size_t, _vp]),
     "vlz_minmax": (ctypes.c_int, [_vp, _i64, _vp, _vp]),
     "vlz_dq_compress_host": (ctypes.c_int, [_vp, _P(Geom), _P(Params), _vp, _vp, _vp, _vp,
                                             _P(Result), ctypes.c_int]),

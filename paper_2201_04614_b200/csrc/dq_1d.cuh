@@ -473,7 +473,7 @@ __global__ void __launch_bounds__(D1_WARPS * 32, VLZ_D1D_MINB)
           // common path: prefix of delta across the block's lanes
           if (lead && c[0] == 0u && bvalid) {  // origin sentinel
             const long long off = offset_of();
-            const long long avail = imax64(0, imin64(cnt, a.n_outliers - off));
+            const long long avail = imax64(0, imin64(cnt, n_outliers_of(a) - off));
             vs[0] = avail > 0 ? a.outliers[off] : 0.f;
             bool qok;
             const int nq = quant_fast(vs[0], a.q, qok);
@@ -503,7 +503,7 @@ __global__ void __launch_bounds__(D1_WARPS * 32, VLZ_D1D_MINB)
           long long off = 0, avail = 0;
           if (smask) {
             off = offset_of();
-            avail = imax64(0, imin64(cnt, a.n_outliers - off));
+            avail = imax64(0, imin64(cnt, n_outliers_of(a) - off));
           }
           int k = excl;
           int acc = 0;
@@ -580,7 +580,7 @@ __global__ void __launch_bounds__(D1_WARPS * 32, VLZ_D1D_MINB)
           sent_acc += run;
           // (a block with no stored and no found outliers needs no offset)
           const long long off = (cnt != 0 || run != 0) ? offset_of() : 0;
-          const long long avail = imax64(0, imin64(cnt, a.n_outliers - off));
+          const long long avail = imax64(0, imin64(cnt, n_outliers_of(a) - off));
           int st = 0;
           if (bad_any) st = 4;
           else if (run > avail) st = 5;

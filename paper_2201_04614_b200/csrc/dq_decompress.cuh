@@ -33,6 +33,7 @@ struct DecompressArgs {
   const void* codes;
   const float* outliers;
   long long n_outliers;
+  const long long* n_out_dev;  // non-null: the stored outlier count lives in device memory
   const int64_t* counts;
   const int64_t* offsets;  // exclusive prefix of counts
   const int64_t* scalars;
@@ -46,6 +47,12 @@ struct DecompressArgs {
   const unsigned int* redo_count;  // tiles queued by the fast kernel
   const long long* redo_list;
 };
+
+// the stream's outlier count: a host value, or a device word written by an
+// earlier kernel (vlz_dq_decompress_dn: no host round trip between calls)
+__device__ __forceinline__ long long n_outliers_of(const DecompressArgs& a) {
+  return a.n_out_dev ? *a.n_out_dev : a.n_outliers;
+}
 
 template <typename CT, int VPL>
 __device__ __forceinline__ void load_codes(const CT* p, bool vec, int nvalid, unsigned (&c)[VPL]) {
@@ -100,7 +107,7 @@ __device__ __forceinline__ void decompress_tile(const DecompressArgs& a, int64_t
     else if (a.mode == MODE_EDGE) s0 = a.scalars[bi * a.nd];
     off = a.offsets[bi];
     const long long cnt = a.counts[bi];
-    avail = imax64(0, imin64(cnt, a.n_outliers - off));
+    avail = imax64(0, imin64(cnt, n_outliers_of(a) - off));
   }
 
   long long grow[VPL];
@@ -282,7 +289,7 @@ __global__ void __launch_bounds__(128) dq_decompress_kernel(DecompressArgs a) {
       const unsigned long long ns = atomicAdd(a.sentinels, 0ull);
       const unsigned long long fb = atomicAdd(a.first_bad, 0ull);
       *a.n_sent_out = (long long)ns;
-      if ((long long)ns != a.n_outliers) {
+      if ((long long)ns != n_outliers_of(a)) {
         *a.status = 7;  // VLZ_ST_SENTINEL_TOTAL
         *a.index = -1;
       } else if (fb != 0x7fffffffffffffffull) {

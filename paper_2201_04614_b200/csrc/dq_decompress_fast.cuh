@@ -217,7 +217,7 @@ __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, c
     else if (a.mode == MODE_BLOCK) s064 = a.scalars[bi];
     else if (a.mode == MODE_EDGE) s064 = a.scalars[bi * a.nd];
     off = a.offsets[bi];
-    avail = imax64(0, imin64(a.counts[bi], a.n_outliers - off));
+    avail = imax64(0, imin64(a.counts[bi], n_outliers_of(a) - off));
   }
   wide |= (s064 >= (1ll << 27)) || (s064 <= -(1ll << 27));
   s0 = (int)s064;

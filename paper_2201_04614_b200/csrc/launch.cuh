@@ -29,6 +29,7 @@ extern std::atomic<long long> g_launches;
 
 int num_sms();
 
+extern std::atomic<int> g_timing;  // per-kernel CUDA-event timing on (vlz_timing)
 // launch with the programmatic-stream-serialization attribute (PDL; the
 // kernels call pdl_enter() first).  VLZ_PDL=0 in the environment disables it.
 bool pdl_enabled();
@@ -44,7 +45,8 @@ inline cudaError_t launch_k(void (*kern)(KArgs...), unsigned grid, unsigned bloc
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  // per-kernel event timing (vlz_timing) brackets exactly one kernel: no PDL then
+  cfg.numAttrs = (pdl_enabled() && !g_timing.load(std::memory_order_relaxed)) ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 

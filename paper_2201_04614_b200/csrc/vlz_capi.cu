@@ -456,10 +456,25 @@ int vlz_dq_compress_finish(const float* d_in, const vlz_geom* g, const vlz_param
                               ws_bytes, static_cast<cudaStream_t>(stream), nullptr, nullptr);
 }
 
+static int decompress_impl(const void* d_codes, bool u32, const float* d_outliers,
+                           int64_t n_outliers, const int64_t* d_n_outliers, const int64_t* d_counts,
+                           const int64_t* d_scalars, const vlz_geom* gg, const vlz_params* p,
+                           float* d_out, vlz_result* d_result, void* d_ws, size_t ws_bytes,
+                           cudaStream_t st);
+
 __attribute__((visibility("hidden"))) int vlz_internal_decompress(const void* d_codes, bool u32, const float* d_outliers,
                            int64_t n_outliers, const int64_t* d_counts, const int64_t* d_scalars,
                            const vlz_geom* gg, const vlz_params* p, float* d_out,
                            vlz_result* d_result, void* d_ws, size_t ws_bytes, cudaStream_t st) {
+  return decompress_impl(d_codes, u32, d_outliers, n_outliers, nullptr, d_counts, d_scalars, gg, p,
+                         d_out, d_result, d_ws, ws_bytes, st);
+}
+
+static int decompress_impl(const void* d_codes, bool u32, const float* d_outliers,
+                           int64_t n_outliers, const int64_t* d_n_outliers, const int64_t* d_counts,
+                           const int64_t* d_scalars, const vlz_geom* gg, const vlz_params* p,
+                           float* d_out, vlz_result* d_result, void* d_ws, size_t ws_bytes,
+                           cudaStream_t st) {
   Geo g;
   if (!make_geo(gg, g) || !valid_params(p) || !d_codes || !d_counts || !d_out || !d_result ||
       !d_ws || n_outliers < 0)
@@ -495,6 +510,7 @@ __attribute__((visibility("hidden"))) int vlz_internal_decompress(const void* d_
   a.codes = d_codes;
   a.outliers = d_outliers;
   a.n_outliers = n_outliers;
+  a.n_out_dev = reinterpret_cast<const long long*>(d_n_outliers);
   a.counts = d_counts;
   a.offsets = w.offsets;
   a.scalars = d_scalars;
@@ -516,6 +532,16 @@ int vlz_dq_decompress(const uint16_t* d_codes, const float* d_outliers, int64_t 
                       size_t ws_bytes, void* stream) {
   return vlz_internal_decompress(d_codes, false, d_outliers, n_outliers, d_counts, d_scalars, g, p, d_out,
                          d_result, d_ws, ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int vlz_dq_decompress_dn(const uint16_t* d_codes, const float* d_outliers,
+                         const int64_t* d_n_outliers, const int64_t* d_counts,
+                         const int64_t* d_scalars, const vlz_geom* g, const vlz_params* p,
+                         float* d_out, vlz_result* d_result, void* d_ws, size_t ws_bytes,
+                         void* stream) {
+  if (!d_n_outliers) return VLZ_E_ARG;
+  return decompress_impl(d_codes, false, d_outliers, 0, d_n_outliers, d_counts, d_scalars, g, p,
+                         d_out, d_result, d_ws, ws_bytes, static_cast<cudaStream_t>(stream));
 }
 
 int vlz_dq_decompress_u32(const uint32_t* d_codes, const float* d_outliers, int64_t n_outliers,

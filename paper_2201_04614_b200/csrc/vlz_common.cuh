@@ -20,13 +20,14 @@ namespace vlz {
 constexpr unsigned FULL = 0xffffffffu;
 
 // Programmatic dependent launch (sm_90+): every kernel of the library waits
-// for its predecessor's completion (and memory) before touching anything,
-// then lets its own successor start launching -- so a kernel's launch and
-// prologue overlap the previous kernel's tail instead of a full launch gap.
-// Both are no-ops for a kernel launched without the PDL attribute.
+// for its predecessor's completion (and memory) before touching anything.
+// The successor is released implicitly when the grid exits (an explicit early
+// launch_dependents let successor CTAs sit on SM resources during the
+// predecessor's tail and measured no better at C5), so what PDL removes is the
+// launch latency between consecutive kernels.  A no-op for a kernel launched
+// without the PDL attribute.
 __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 // Division of 32-bit unsigned values by a launch-invariant divisor d >= 1

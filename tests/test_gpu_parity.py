@@ -310,3 +310,48 @@ def test_fast_kernels_large_blocks(oracle, shape, b):
                     (1e-3, "mean:edge"), (1e-3, "min:global")):
         s = _check_full(oracle, data, eb, b, pol, 512)
         assert s.outlier_values.size > 0
+
+
+def test_decompress_with_device_outlier_count():
+    # vlz_dq_decompress_dn reads the stored outlier count from the compressor's
+    # device result block: same output and same corrupt-stream verdict as the
+    # host-count entry point, with no host round trip between the two calls
+    import ctypes
+
+    from paper_2201_04614_b200 import _lib
+
+    lib = _lib.load()
+    cases = [(workloads.gen_c3(shape=(64, 96, 128)), 8, "mean:global"),
+             (workloads.gen_c3(shape=(48, 80, 200)), 16, "max:block"),
+             ((np.cumsum(np.random.default_rng(2).normal(0, 1, (1 << 22) + 777)) * 0.01)
+              .astype(np.float32), 64, "zero")]
+    for data, b, pol in cases:
+        eb = workloads.value_range_eb(data, 1e-4)
+        cfg = _cfg(eb, b, pol, 512)
+        x = torch.from_numpy(data).cuda()
+        dev = gpu.compress_device(x, cfg, eb=eb).check()
+        ref = gpu.decompress_device(dev.codes, dev.outliers, dev.n_outliers, dev.counts,
+                                    dev.scalars, dev.grid, eb, 512, cfg.padding)
+        g = _lib.geom(dev.grid.descriptor.dims, b)
+        p = _lib.params(eb, 512, cfg.padding.kind_code, cfg.padding.gran_code)
+        wsb = lib.vlz_workspace_size(ctypes.byref(g))
+        ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+        out = torch.empty_like(x)
+        res = torch.empty(8, dtype=torch.int64, device="cuda")
+        sc = dev.scalars.data_ptr() if dev.scalars.numel() else None
+        stream = torch.cuda.current_stream().cuda_stream
+        rc = lib.vlz_dq_decompress_dn(dev.codes.data_ptr(), dev.outliers.data_ptr(),
+                                      dev.result[2:3].data_ptr(), dev.counts.data_ptr(), sc,
+                                      ctypes.byref(g), ctypes.byref(p), out.data_ptr(),
+                                      res.data_ptr(), ws.data_ptr(), wsb, stream)
+        assert rc == 0
+        assert int(res[0].item()) == 0
+        assert torch.equal(out, ref)
+        # a stored count one short: the sentinel-total verdict, as with a host count
+        short = dev.result.clone()
+        short[2] -= 1
+        rc = lib.vlz_dq_decompress_dn(dev.codes.data_ptr(), dev.outliers.data_ptr(),
+                                      short[2:3].data_ptr(), dev.counts.data_ptr(), sc,
+                                      ctypes.byref(g), ctypes.byref(p), out.data_ptr(),
+                                      res.data_ptr(), ws.data_ptr(), wsb, stream)
+        assert rc == 0 and int(res[0].item()) == _lib.ST_SENTINEL_TOTAL
