@@ -49,12 +49,17 @@ struct DFastShape {
   // stage layout [row][lane] x VPL codes: every lane copies (cp.async) and
   // later reads its own VPL codes of each row -- conflict-free, no barrier
   static constexpr int LANE_BYTES = VPL * 2;
-  static constexpr int STAGE_BYTES = S::BY * 32 * LANE_BYTES;
+  // a plane streams in SPLIT stages of STAGE_ROWS rows (b >= 32: 8-row
+  // stages, so the ring stays small enough for several CTAs per SM)
+  static constexpr int SPLIT = S::BY >= 32 ? S::BY / 8 : 1;
+  static constexpr int STAGE_ROWS = S::BY / SPLIT;
+  static constexpr int STAGE_BYTES = STAGE_ROWS * 32 * LANE_BYTES;
+  static constexpr int PLANE_BYTES = S::BY * 32 * LANE_BYTES;
   static constexpr int PREV_BYTES = (ND == 3) ? S::BY * S::W * 4 : 0;
-  // edge tiles fill their codes synchronously into a slot of their own, so
-  // the ring of interior planes keeps streaming underneath
+  // edge tiles fill a whole plane of codes synchronously into a slot of their
+  // own, so the ring of interior planes keeps streaming underneath
   static constexpr int EDGE_OFF = DSTAGES * STAGE_BYTES + PREV_BYTES;
-  static constexpr int WARP_SMEM = EDGE_OFF + STAGE_BYTES;
+  static constexpr int WARP_SMEM = EDGE_OFF + PLANE_BYTES;
   // per-warp footprint of a kernel variant (the edge slot only when it has edge tiles)
   __host__ __device__ static constexpr int warp_smem(bool edges) { return edges ? WARP_SMEM : EDGE_OFF; }
 };
@@ -86,7 +91,7 @@ struct DProducer {
   using F = DFastShape<ND, B, VPL>;
   static constexpr bool TMAP = false;
   uint32_t tile;
-  int zl, ez;
+  int zl, ez, part;
   const uint16_t* src;  // this lane's codes in plane 0, row 0 of the current tile
   int stage;
 
@@ -103,6 +108,7 @@ struct DProducer {
         src = codes + block_start(g, c.bz, c.by, bx0, S::BZ, S::BY, S::BX, ez, S::BY) +
               (int64_t)blk * ez * F::SLICE_CODES + (lane * VPL) % S::BX;
         zl = 0;
+        part = 0;
         return;
       }
       tile += nwarps;
@@ -118,13 +124,16 @@ struct DProducer {
                                         unsigned char* ring, uint32_t nwarps, int lane) {
     if (tile < (uint32_t)g.ntiles) {
       unsigned char* dst = ring + stage * F::STAGE_BYTES + lane * F::LANE_BYTES;
-      const uint16_t* s = src + (int64_t)zl * F::SLICE_CODES;
+      const uint16_t* s = src + (int64_t)zl * F::SLICE_CODES + part * F::STAGE_ROWS * S::BX;
 #pragma unroll
-      for (int yl = 0; yl < S::BY; ++yl)
+      for (int yl = 0; yl < F::STAGE_ROWS; ++yl)
         cp_async<F::LANE_BYTES>(dst + yl * 32 * F::LANE_BYTES, s + yl * S::BX);
-      if (++zl >= ez) {
-        tile += nwarps;
-        seek(g, codes, nwarps, lane);
+      if (++part == F::SPLIT) {
+        part = 0;
+        if (++zl >= ez) {
+          tile += nwarps;
+          seek(g, codes, nwarps, lane);
+        }
       }
     }
     cp_async_commit();
@@ -275,6 +284,14 @@ __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, c
     float* dst = orow;
 #pragma unroll 2
     for (int yl = 0; yl < ey; ++yl) {
+      if constexpr (!EDGE && !TMAP && F::SPLIT > 1) {
+        if (yl > 0 && yl % F::STAGE_ROWS == 0) {  // next stage of this plane
+          prod.issue(g, codes, ring, nwarps, lane);
+          cons.advance();
+          slot = slot0 + cons.stage * F::STAGE_BYTES;
+          cp_async_wait<DSTAGES - 1>();
+        }
+      }
       unsigned c[VPL];
       const unsigned char* rowp = slot;
       if (TMAP && !EDGE)  // block blk, row yl: 16-byte chunk yl of line blk, XOR-swizzled
