@@ -355,3 +355,28 @@ def test_decompress_with_device_outlier_count():
                                       ctypes.byref(g), ctypes.byref(p), out.data_ptr(),
                                       res.data_ptr(), ws.data_ptr(), wsb, stream)
         assert rc == 0 and int(res[0].item()) == _lib.ST_SENTINEL_TOTAL
+
+
+@pytest.mark.parametrize("shape,b", [(((1 << 22) + 5000,), 64), (((1 << 22) + 5000,), 256),
+                                     ((40, 64, 256), 32), ((96, 96, 128), 64), ((300, 512), 64)])
+def test_fused_kernels_error_precedence(shape, b):
+    # quantize.py:58-72 through the fused 1-D / large-block kernels: the first
+    # non-finite value wins over an earlier overflow; else the first overflow
+    rng = np.random.default_rng(7)
+    base = rng.uniform(-1, 1, shape).astype(np.float32)
+    flat = base.reshape(-1)
+    n = flat.size
+    ovf_at, nan_at = n // 3, (2 * n) // 3
+    eb = 1e-6
+    d = flat.copy()
+    d[ovf_at] = 1.0e5  # |v / 2eb| = 5e10 >= 2^31 - 1
+    d[nan_at] = np.nan
+    with pytest.raises(ConfigError) as err:
+        dualquant_vector(d.reshape(shape), _cfg(eb, b, "mean:global", 512))
+    assert str(nan_at) in str(err.value)
+    d2 = flat.copy()
+    d2[ovf_at] = 1.0e5
+    d2[n - 1] = -2.0e5
+    with pytest.raises(BoundTooSmallError) as err:
+        dualquant_vector(d2.reshape(shape), _cfg(eb, b, "zero", 512))
+    assert err.value.index == ovf_at
