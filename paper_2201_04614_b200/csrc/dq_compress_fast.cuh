@@ -269,7 +269,19 @@ __device__ __forceinline__ void fast_tile(const FastArgs& fa, uint32_t tile, con
     for (int part = 0; part < F::SPLIT; ++part) {
     const float* plane = ring + cons.stage * F::STAGE_FLOATS + lane * VPL;
     unsigned char* const stage_bytes = reinterpret_cast<unsigned char*>(ring + cons.stage * F::STAGE_FLOATS);
+    const uint32_t stage_s = smem_u32(stage_bytes);
     mbar_wait(&bars[cons.stage], cons.parity);
+    if (zl == 0 && part == 0) {
+      // the block origins sit in row 0 of the layer's first stage: take their
+      // value and prequantized d here, once per tile, instead of a predicated
+      // capture in every row (same quant_fast / quant_exact decision as the row)
+      v_origin = plane[0];
+      bool fok, ob = false, oo;
+      int n0 = quant_fast(v_origin, q, fok);
+      if (!fok) n0 = quant_exact(v_origin, q, ob, oo);
+      d_origin = n0;
+      bad_origin = ob;
+    }
 #pragma unroll 2
     for (int r = 0; r < F::STAGE_ROWS; ++r) {
       const int yl = part * F::STAGE_ROWS + r;
@@ -364,12 +376,6 @@ __device__ __forceinline__ void fast_tile(const FastArgs& fa, uint32_t tile, con
         u[j] = (unsigned)(dl[j] + (R - 1));
         umax = u[j] > umax ? u[j] : umax;
       }
-      const bool origin_row = (zl == 0) && (yl == 0) && xhead;
-      if (origin_row) {
-        d_origin = (int)(nb[0] - MAGIC_BITS);
-        bad_origin = badm & 1u;
-        v_origin = v[0];
-      }
       unsigned cadd = 0x00010001u;  // per 16-bit half: code = u + 1
       if (__any_sync(FULL, umax > span || badm != 0u)) {
         // rare: outliers (code 0; narrowing failures included), ranked inside
@@ -383,7 +389,7 @@ __device__ __forceinline__ void fast_tile(const FastArgs& fa, uint32_t tile, con
         }
         cadd = 0u;
         om &= vmask;
-        if (origin_row) om &= ~1u;
+        if ((zl == 0) && (yl == 0) && xhead) om &= ~1u;  // the origin is settled at the tile end
         int tot;
         const int excl = group_excl_scan<LPB>(__popc(om), lane, tot);
         int k = run + excl;
@@ -398,8 +404,18 @@ __device__ __forceinline__ void fast_tile(const FastArgs& fa, uint32_t tile, con
         // rotated by row: conflict-free here and in the copy-out below)
         constexpr int CPR = W / 8;
         const int pos = (stage_chunk0 + r * (BX / 8)) & (CPR - 1);
-        st_codes<VPL>(reinterpret_cast<uint16_t*>(stage_bytes + r * W * 4 + pos * 16 +
-                                                  stage_sub), u, cadd);
+        // 32-bit shared address (st.shared): no generic-to-shared window
+        // arithmetic per row
+        const uint32_t sa = stage_s + (uint32_t)(r * W * 4 + pos * 16 + stage_sub);
+        if constexpr (VPL == 4) {
+          asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(sa),
+                       "r"(__byte_perm(u[0], u[1], 0x5410) + cadd),
+                       "r"(__byte_perm(u[2], u[3], 0x5410) + cadd)
+                       : "memory");
+        } else {
+          st_codes<VPL>(reinterpret_cast<uint16_t*>(stage_bytes + r * W * 4 + pos * 16 +
+                                                    stage_sub), u, cadd);
+        }
       } else if (vec_store) {
         st_codes<VPL>(cptr, u, cadd);
       } else if (lane_valid) {
