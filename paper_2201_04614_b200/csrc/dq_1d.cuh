@@ -509,12 +509,18 @@ __global__ void __launch_bounds__(D1_WARPS * 32, VLZ_D1D_MINB)
           int acc = 0;
           unsigned before = 0;
           bool reset = false;
+          // the row's outlier loads first (in flight together), then the resets
 #pragma unroll
           for (int j = 0; j < VPL; ++j) {
             vs[j] = 0.f;
             if ((smask >> j) & 1u) {
-              if (k < avail) vs[j] = a.outliers[off + k];
+              if (k < avail) vs[j] = __ldg(a.outliers + off + k);
               ++k;
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < VPL; ++j) {
+            if ((smask >> j) & 1u) {
               bool qok;
               const int nq = quant_fast(vs[j], a.q, qok);
               const long long ds = qok ? (long long)nq : quant_value(vs[j], a.q.twoeb);

@@ -353,12 +353,19 @@ __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, c
         int acc = 0;
         unsigned before = 0;
         bool reset = false;
+        // all of the row's outlier loads first (independent addresses), so
+        // they are in flight together, then the quantisation and the resets
 #pragma unroll
         for (int j = 0; j < VPL; ++j) {
           vs[j] = 0.f;
           if ((smask >> j) & 1u) {
-            if (k < avail) vs[j] = a.outliers[off + k];
+            if (k < avail) vs[j] = __ldg(a.outliers + off + k);
             ++k;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < VPL; ++j) {
+          if ((smask >> j) & 1u) {
             // the compress side's exact-fast quotient (quant_fast: equal to
             // round_half_away(fl64(v / 2eb)) whenever it reports ok); the fp64
             // division only for the rest
