@@ -162,14 +162,22 @@ __device__ __forceinline__ void decompress_tile(const DecompressArgs& a, int64_t
         int tot;
         const int excl = group_excl_scan<LPB>(__popc(sm), lane, tot);
         int k = run + excl;
+        // loads first (in flight together), then the exact-fast quotient
 #pragma unroll
         for (int j = 0; j < VPL; ++j) {
           vs[j] = 0.f;
+          if ((sm >> j) & 1u) {
+            if (k < avail) vs[j] = __ldg(a.outliers + off + k);
+            ++k;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < VPL; ++j) {
           hs[j] = 0;
           if ((sm >> j) & 1u) {
-            if (k < avail) vs[j] = a.outliers[off + k];
-            ++k;
-            const long long ds = quant_value(vs[j], a.q.twoeb);
+            bool qok;
+            const int nq = quant_fast(vs[j], a.q, qok);
+            const long long ds = qok ? (long long)nq : quant_value(vs[j], a.q.twoeb);
             hs[j] = (ds - s0) - ep[j] - gp[j];
           }
         }
