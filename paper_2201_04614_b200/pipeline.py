@@ -39,13 +39,44 @@ def _device():
     return torch.device("cuda", torch.cuda.current_device())
 
 
+_H2D_CHUNK = 1 << 24  # float32 elements (64 MB) per pinned staging buffer
+
+
+def _to_device(data: np.ndarray, device) -> torch.Tensor:
+    """Host array -> device tensor through two pinned staging buffers: the
+    (multi-threaded) copy of chunk i into one overlaps the DMA of chunk i-1
+    from the other (a pageable .to() runs at ~11 GB/s)."""
+    src = torch.from_numpy(np.ascontiguousarray(data)).reshape(-1)
+    n = src.numel()
+    x = torch.empty(n, dtype=src.dtype, device=device)
+    if n <= _H2D_CHUNK // 4:
+        x.copy_(src)
+        return x.view(data.shape)
+    stream = torch.cuda.current_stream(device)
+    bufs = [torch.empty(_H2D_CHUNK, dtype=src.dtype, pin_memory=True) for _ in range(2)]
+    done = [None, None]
+    for i, s0 in enumerate(range(0, n, _H2D_CHUNK)):
+        k = i & 1
+        m = min(_H2D_CHUNK, n - s0)
+        if done[k] is not None:
+            done[k].synchronize()  # the DMA out of this buffer has finished
+        bufs[k][:m].copy_(src[s0:s0 + m])
+        x[s0:s0 + m].copy_(bufs[k][:m], non_blocking=True)
+        done[k] = torch.cuda.Event()
+        done[k].record(stream)
+    for e in done:
+        if e is not None:
+            e.synchronize()  # staging buffers return to the caching host allocator
+    return x.view(data.shape)
+
+
 def _compress(data: np.ndarray, config: CompressionConfig, want_stream: bool):
     desc = ArrayDescriptor.from_array(data)
     eb = resolve_error_bound(config.error_bound, data)
     grid = build_block_grid(desc, config.block_edge)
     if eb <= 0.0:
         raise ConfigError(f"resolved error bound must be > 0, got {eb}")
-    x = torch.from_numpy(np.ascontiguousarray(data)).to(_device())
+    x = _to_device(data, _device())
     dev = gpu.compress_device(x, config, eb=eb)
     try:
         dev.check()
