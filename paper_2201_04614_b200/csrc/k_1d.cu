@@ -6,10 +6,8 @@ namespace vlz {
 
 template <typename Kern>
 static cudaError_t d1_grid(Kern kern, int smem, int64_t ntiles1, int64_t& grid) {
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, D1_WARPS * 32, smem);
+  cudaError_t e = occupancy(kern, D1_WARPS * 32, smem, per_sm);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
   grid = (int64_t)per_sm * num_sms();

@@ -55,10 +55,8 @@ static cudaError_t run_d(bool u32, const DecompressArgs& a, cudaStream_t st) {
           fsmem = edges ? dtma_smem_bytes<ND, B, VPL, true>() : dtma_smem_bytes<ND, B, VPL, false>();
         }
       }
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem);
-      if (e != cudaSuccess) return e;
       int per_sm = 0;
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, FAST_WARPS * 32, fsmem);
+      cudaError_t e = occupancy(kern, FAST_WARPS * 32, fsmem, per_sm);
       if (e != cudaSuccess) return e;
       if (per_sm < 1) per_sm = 1;
       int64_t grid = (int64_t)per_sm * num_sms();
@@ -75,7 +73,8 @@ static cudaError_t run_d(bool u32, const DecompressArgs& a, cudaStream_t st) {
       if (e != cudaSuccess) return e;
       auto redo = dq_decompress_kernel<ND, B, VPL, uint16_t, true>;
       if (smem > 48 * 1024) {
-        e = cudaFuncSetAttribute(redo, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        int rps = 0;
+        e = occupancy(redo, 128, smem, rps);  // (its smem opt-in, once)
         if (e != cudaSuccess) return e;
       }
       if (t) timing_mark(TK_REDO, true, st);

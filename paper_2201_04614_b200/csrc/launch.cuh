@@ -30,6 +30,16 @@ extern std::atomic<long long> g_launches;
 int num_sms();
 
 extern std::atomic<int> g_timing;  // per-kernel CUDA-event timing on (vlz_timing)
+// Resident CTAs per SM of a kernel at (block, dynamic smem), with the
+// dynamic-smem opt-in done first -- both once per (kernel, device, config):
+// the driver queries cost microseconds per call, which launch-bound small
+// arrays would pay on every compress/decompress.
+cudaError_t occupancy_cached(const void* kern, int block, int smem, int& per_sm);
+template <typename... KArgs>
+inline cudaError_t occupancy(void (*kern)(KArgs...), int block, int smem, int& per_sm) {
+  return occupancy_cached(reinterpret_cast<const void*>(kern), block, smem, per_sm);
+}
+
 // launch with the programmatic-stream-serialization attribute (PDL; the
 // kernels call pdl_enter() first).  VLZ_PDL=0 in the environment disables it.
 bool pdl_enabled();
@@ -60,12 +70,8 @@ void timing_mark(int kind, bool start, cudaStream_t st);
 template <typename Kern, typename Arg>
 inline cudaError_t launch_tiles(Kern kernel, int64_t ntiles, int smem, cudaStream_t st,
                                 const Arg& arg) {
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-  }
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 128, smem);
+  cudaError_t e = occupancy(kernel, 128, smem, per_sm);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
   int64_t grid = (int64_t)per_sm * num_sms();

@@ -61,10 +61,8 @@ cudaError_t run_compress_shape(const CompressArgs& a, cudaStream_t st) {
                        FastShape<ND, B, VPL>::STAGE_ROWS)) {
       auto kern = dq_compress_fast_kernel<ND, B, VPL, MODE, K>;
       constexpr int fsmem = fast_smem_bytes<ND, B, VPL>();
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem);
-      if (e != cudaSuccess) return e;
       int per_sm = 0;
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, FAST_WARPS * 32, fsmem);
+      cudaError_t e = occupancy(kern, FAST_WARPS * 32, fsmem, per_sm);
       if (e != cudaSuccess) return e;
       if (per_sm < 1) per_sm = 1;
       int64_t grid = (int64_t)per_sm * num_sms();
@@ -85,7 +83,8 @@ cudaError_t run_compress_shape(const CompressArgs& a, cudaStream_t st) {
       // int64 redo of tiles whose |d| reached 2^24 (usually none: exits at once)
       auto redo = dq_compress_kernel<ND, B, VPL, MODE, true>;
       if (smem > 48 * 1024) {
-        e = cudaFuncSetAttribute(redo, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        int rps = 0;
+        e = occupancy(redo, 128, smem, rps);  // (its smem opt-in, once)
         if (e != cudaSuccess) return e;
       }
       if (t) timing_mark(TK_REDO, true, st);

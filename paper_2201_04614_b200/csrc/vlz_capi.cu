@@ -10,6 +10,8 @@
 
 #include <atomic>
 #include <cstdio>
+#include <tuple>
+#include <map>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -55,6 +57,32 @@ void timing_mark(int kind, bool start, cudaStream_t st) {
   } else {
     g_trecs.push_back({kind, g_open[kind], e});
   }
+}
+
+cudaError_t occupancy_cached(const void* kern, int block, int smem, int& per_sm) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, int, int>, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(kern, dev, block, smem);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      per_sm = it->second;
+      return cudaSuccess;
+    }
+  }
+  if (smem > 48 * 1024) {
+    const cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+  }
+  const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, block, smem);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  cache[key] = per_sm;
+  return cudaSuccess;
 }
 
 bool pdl_enabled() {
