@@ -305,7 +305,7 @@ def run_ours(args):
     # launch stream (the roofline's kernel durations come from the same pass;
     # kernels are launched without PDL while this timing is on)
     l0 = lib.vlz_launch_count()
-    lib.vlz_timing(1)
+    lib.vlz_timing(0 if os.environ.get("VLZ_BENCH_KTIMING") == "0" else 1)
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
@@ -348,7 +348,7 @@ def run_ours(args):
     alg = 6.0 * n + 4.0 * n_out + 8.0 * nb + 8.0
     dom = "compress" if k1 >= k4 else "decompress"
     kt = (k1 if dom == "compress" else k4) / K
-    achieved = alg / (kt * 1e-3) / 1e9
+    achieved = alg / (kt * 1e-3) / 1e9 if kt > 0 else 0.0  # (VLZ_BENCH_KTIMING=0: no kernel times)
     traffic = load_traffic(dom)
 
     e2e = None
