@@ -254,9 +254,10 @@ def run_ours(args):
                                        codes.data_ptr(), counts.data_ptr(), scalars.data_ptr(),
                                        res.data_ptr(), stats.data_ptr(), wspace.data_ptr(), wsb, sp)
         assert rc == 0
-        if ws > 1:
-            dist.all_reduce(stats[0:2], op=dist.ReduceOp.SUM)
-            dist.all_reduce(stats[2:4], op=dist.ReduceOp.MIN)
+        if ws > 1:  # padding statistics of all shards: one all-gather, reduced locally
+            from paper_2201_04614_b200.sharded import reduce_stats
+
+            reduce_stats(stats)
         rc = lib.vlz_dq_compress_finish(x.data_ptr(), ctypes.byref(g), ctypes.byref(p),
                                         stats.data_ptr(), codes.data_ptr(), outl.data_ptr(),
                                         counts.data_ptr(), scalars.data_ptr(), res.data_ptr(),

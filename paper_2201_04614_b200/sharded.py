@@ -75,13 +75,17 @@ def _reduce_range(lo: float, hi: float, group, device):
 
 
 def reduce_stats(stats: torch.Tensor, group=None):
-    """In place: [sum, count] summed, [min, -max] minimised across ranks."""
-    head = stats[0:2].clone()
-    tail = stats[2:4].clone()
-    dist.all_reduce(head, op=dist.ReduceOp.SUM, group=group)
-    dist.all_reduce(tail, op=dist.ReduceOp.MIN, group=group)
-    stats[0:2] = head
-    stats[2:4] = tail
+    """In place: [sum, count] summed, [min, -max] minimised across ranks.
+
+    One collective per step: an all-gather of every rank's 4 words (32 B),
+    reduced locally, instead of a SUM and a MIN all-reduce (each collective
+    costs a launch-latency-bound round trip at 8 GPUs)."""
+    world = dist.get_world_size(group)
+    allst = torch.empty(world * 4, dtype=stats.dtype, device=stats.device)
+    dist.all_gather_into_tensor(allst, stats.contiguous(), group=group)
+    allst = allst.view(world, 4)
+    stats[0:2] = allst[:, 0:2].sum(dim=0)  # int64 wraps like the reference's np.sum
+    stats[2:4] = allst[:, 2:4].min(dim=0).values
     return stats
 
 
