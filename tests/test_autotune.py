@@ -77,19 +77,24 @@ def test_csv_rows_and_apply_chosen():
     assert (cfg.block_edge, cfg.lane_width) == (16, 4)
 
 
-@pytest.mark.parametrize("shape,b", [((1000,), 64), ((33, 47), 16), ((20, 17, 9), 8)])
+@pytest.mark.parametrize("shape,b", [((1000,), 64), ((33, 47), 16), ((20, 17, 9), 8), ((9, 40, 70), 8), ((70, 9, 33), 16)])
 def test_gather_block_column(shape, b):
     rng = np.random.default_rng(5)
     x = torch.from_numpy(rng.standard_normal(shape).astype(np.float32))
     grid = build_block_grid(ArrayDescriptor.from_array(x), b)
     picks = sample_blocks(grid, 0.5, 2)
     col = gather_block_column(x, grid, picks)
-    assert col.shape == (len(picks) * b,) + (b,) * (len(shape) - 1)
+    k, nd = len(picks), len(shape)
+    c = k if nd == 1 else min(k, grid.blocks_per_dim[-1])
+    r = -(-k // c)
+    want = (k * b,) if nd == 1 else (r * b,) + (b,) * (nd - 2) + (c * b,)
+    assert col.shape == want
     cgrid = build_block_grid(ArrayDescriptor.from_array(col), b)
-    assert cgrid.block_count == len(picks)
-    for i, bi in enumerate(picks):
-        ext = grid.block_extents(int(bi))
-        src = x[tuple(slice(o, o + e) for o, e in zip(grid.block_origin(int(bi)), ext))]
+    assert cgrid.block_count == (k if nd == 1 else r * c)
+    for i in range(cgrid.block_count):
+        bi = int(picks[i % k])
+        ext = grid.block_extents(bi)
+        src = x[tuple(slice(o, o + e) for o, e in zip(grid.block_origin(bi), ext))]
         blk = col[tuple(slice(o, o + b) for o in cgrid.block_origin(i))]
         assert torch.equal(blk[tuple(slice(0, e) for e in ext)], src)
         assert float(blk.abs().sum()) == pytest.approx(float(src.abs().sum()), rel=1e-5)
