@@ -170,14 +170,23 @@ int vlz_huff_decode(const uint8_t* payload, int64_t nbytes, int64_t bit_length,
   if (nbytes * 8 < bit_length) return 2;
   int maxlen = 0;
   for (int i = 0; i < nsym; ++i) maxlen = lens[i] > maxlen ? lens[i] : maxlen;
-  std::vector<uint64_t> first_code(maxlen + 2, 0), first_idx(maxlen + 2, 0), cnt(maxlen + 2, 0);
+  // first_code grows without bound for an over-subscribed book (Kraft sum
+  // > 1, reachable from a crafted container); the reference computes it in
+  // Python ints.  Saturating at 2^70 keeps every comparison with a <= 64-bit
+  // prefix exact: a saturated first code is above any prefix, as the true one is.
+  using u128 = unsigned __int128;
+  const u128 kCap = (u128)1 << 70;
+  std::vector<u128> first_code(maxlen + 2, 0);
+  std::vector<uint64_t> first_idx(maxlen + 2, 0), cnt(maxlen + 2, 0);
   for (int i = 0; i < nsym; ++i) cnt[lens[i]] += 1;
   {
-    uint64_t code = 0, idx = 0;
+    u128 code = 0;
+    uint64_t idx = 0;
     for (int l = 1; l <= maxlen; ++l) {
       first_code[l] = code;
       first_idx[l] = idx;
       code = (code + cnt[l]) << 1;
+      if (code > kCap) code = kCap;
       idx += cnt[l];
     }
   }
@@ -186,13 +195,18 @@ int vlz_huff_decode(const uint8_t* payload, int64_t nbytes, int64_t bit_length,
   std::vector<uint16_t> lut_sym(1u << lut_bits, 0);
   std::vector<uint8_t> lut_len(1u << lut_bits, 0);
   {
-    std::vector<uint64_t> cw(nsym);
-    codewords(lens, nsym, cw.data());
-    for (int i = 0; i < nsym; ++i) {
-      if (lens[i] > lut_bits) continue;
-      const uint64_t base = cw[i] << (lut_bits - lens[i]);
+    // canonical codewords in (length, symbol) order; an over-subscribed book
+    // runs its codewords past the table, where the reference's slice
+    // assignment (huffman.py:166-167) truncates -- so do we
+    const uint64_t size = 1ull << lut_bits;
+    uint64_t code = 0;
+    for (int i = 0; i < nsym && lens[i] <= lut_bits; ++i) {
+      if (i && lens[i] < lens[i - 1]) break;  // not canonical order: table stays partial
+      if (i) code = (code + 1) << (lens[i] - lens[i - 1]);
+      if (code >= (size >> (lut_bits - lens[i]))) break;  // later codewords lie further out
+      const uint64_t base = code << (lut_bits - lens[i]);
       const uint64_t span = 1ull << (lut_bits - lens[i]);
-      for (uint64_t k = 0; k < span; ++k) {
+      for (uint64_t k = 0; k < span && base + k < size; ++k) {
         lut_sym[base + k] = syms[i];
         lut_len[base + k] = lens[i];
       }
@@ -212,7 +226,9 @@ int vlz_huff_decode(const uint8_t* payload, int64_t nbytes, int64_t bit_length,
         continue;
       }
     }
-    uint64_t acc = 0;
+    // a prefix of more than 64 bits (lengths up to 255 are representable)
+    // saturates at 2^64: every first code that can match lies below it
+    u128 acc = 0;
     int acclen = 0;
     for (;;) {
       if (bp >= total_bits) {
@@ -220,13 +236,14 @@ int vlz_huff_decode(const uint8_t* payload, int64_t nbytes, int64_t bit_length,
         return 3;
       }
       acc = (acc << 1) | bit_at(bp++);
+      if (acc > ((u128)1 << 64)) acc = (u128)1 << 64;
       ++acclen;
       if (acclen > maxlen) {
         *consumed_out = bp;
         return 4;
       }
-      const uint64_t off = acc - first_code[acclen];
-      if (acc >= first_code[acclen] && off < cnt[acclen]) {
+      if (acc >= first_code[acclen] && (uint64_t)(acc - first_code[acclen]) < cnt[acclen]) {
+        const uint64_t off = (uint64_t)(acc - first_code[acclen]);
         out[i] = syms[first_idx[acclen] + off];
         break;
       }

@@ -178,7 +178,7 @@ __device__ void decode_run(const HDArgs& a, const HDMeta& m, int64_t k, long lon
       len = 0;
       for (int l = 13; l <= m.maxlen; ++l) {
         const unsigned long long code = win >> (64 - l);
-        if (code < m.end[l]) {
+        if (code < m.end[l] && code >= m.first_code[l]) {
           len = l;
           sym = syms[m.first_idx[l] + (unsigned)(code - m.first_code[l])];
           break;
@@ -420,13 +420,19 @@ int vlz_huff_decode_device(const uint8_t* d_payload, int64_t nbytes, int64_t bit
   if (maxlen > vlz::HD_MAXLEN) return VLZ_E_ARG;
   for (int i = 0; i < nsym; ++i) meta.cnt[h_lens[i]] += 1;
   {
+    // An over-subscribed book (Kraft sum > 1, possible in a crafted
+    // container) grows the first codes past 2^l; the reference works in
+    // Python ints.  Saturating at 2^60 (> 2^HD_MAXLEN) and clamping end[l] to
+    // 2^l leave every test `prefix_l < end[l]` as it is in exact arithmetic.
+    const unsigned long long cap = 1ull << 60;
     unsigned long long code = 0;
     unsigned idx = 0;
     for (int l = 1; l <= maxlen; ++l) {
       meta.first_code[l] = code;
       meta.first_idx[l] = idx;
-      meta.end[l] = code + meta.cnt[l];
-      code = (code + meta.cnt[l]) << 1;
+      const unsigned long long e = code + meta.cnt[l];
+      meta.end[l] = e < (1ull << l) ? e : (1ull << l);
+      code = e << 1 < cap ? e << 1 : cap;
       idx += meta.cnt[l];
     }
   }
@@ -438,15 +444,18 @@ int vlz_huff_decode_device(const uint8_t* d_payload, int64_t nbytes, int64_t bit
     unsigned long long code = 0;
     for (int i = 0; i < nsym; ++i) {
       const int L = h_lens[i];
-      if (L <= 12) {
+      if (L <= 12 && code < (4096ull >> (12 - L))) {
+        // codewords past the table (over-subscribed book) are dropped, as the
+        // reference's slice assignment truncates them (huffman.py:166-167)
         const unsigned long long b0 = code << (12 - L);
-        for (unsigned long long t = 0; t < (1ull << (12 - L)); ++t) {
+        for (unsigned long long t = 0; t < (1ull << (12 - L)) && b0 + t < 4096; ++t) {
           len12[b0 + t] = (unsigned char)L;
           sym12[b0 + t] = h_syms[i];
         }
       }
       code += 1;
-      if (i + 1 < nsym) code <<= (int)h_lens[i + 1] - L;
+      if (i + 1 < nsym) code = h_lens[i + 1] > 12 ? 4096 : code << ((int)h_lens[i + 1] - L);
+      if (code > 4096) code = 4096;
     }
     for (unsigned v = 0; v < 4096; ++v) {
       const int L1 = len12[v];

@@ -27,6 +27,7 @@ from .model import (
     CompressionConfig,
     ErrorBound,
     ErrorBoundMode,
+    PaddingGranularity,
     PaddingPolicy,
     PaddingValue,
     build_block_grid,
@@ -53,6 +54,24 @@ def value_range(x: torch.Tensor, stream=None):
         raise RuntimeError(f"vlz_minmax failed ({rc})")
     lo, hi = out.tolist()
     return lo, hi
+
+
+def check_resolved_eb(eb: float, data) -> None:
+    """quantize.py:58-64 on a resolved bound.  A NaN bound comes from a
+    value-range-relative bound over data holding NaN (or both infinities):
+    the reference's `eb <= 0` test lets it through and its non-finite scan
+    names the first such element, so the same ConfigError is raised here
+    (the scan runs on the device for a CUDA tensor)."""
+    if eb > 0.0:
+        return
+    if eb != eb:
+        if isinstance(data, torch.Tensor):
+            bad = ~torch.isfinite(data.reshape(-1))
+            idx = int(torch.argmax(bad.to(torch.uint8)).item())
+        else:
+            idx = int(np.argmin(np.isfinite(np.asarray(data).ravel())))
+        raise ConfigError(f"data contains a non-finite value at flat index {idx}")
+    raise ConfigError(f"resolved error bound must be > 0, got {eb}")
 
 
 def resolve_eb_device(eb: ErrorBound, x: torch.Tensor) -> float:
@@ -96,8 +115,19 @@ class DeviceCodeStream:
     def n_outliers(self) -> int:
         return int(self.read_result().n_outliers)
 
-    def check(self) -> "DeviceCodeStream":
+    def check(self, scalar_order: bool = False) -> "DeviceCodeStream":
+        """Raise the reference's exception for a failed compress.  The vector
+        path (quantize.py:60-72) reports any non-finite value before any
+        overflow; the scalar kernel at lane width 1 (kernel.py:138-145) checks
+        element by element, so the smaller flat index decides
+        (`scalar_order=True`).  first_overflow counts non-finite values too."""
         r = self.read_result()
+        if scalar_order and r.status in (_lib.ST_NONFINITE, _lib.ST_OVERFLOW):
+            first = min(int(r.first_nonfinite), int(r.first_overflow))
+            if first == int(r.first_nonfinite):
+                raise ConfigError(f"data contains a non-finite value at flat index {first}")
+            v = float(self.source.reshape(-1)[first].item()) if self.source is not None else float("nan")
+            raise BoundTooSmallError(first, v, self.eb)
         if r.status == _lib.ST_NONFINITE:
             raise ConfigError(f"data contains a non-finite value at flat index {r.index}")
         if r.status == _lib.ST_OVERFLOW:
@@ -143,8 +173,7 @@ def compress_device(x: torch.Tensor, config: CompressionConfig, eb: float = None
         raise ConfigError("block edge 256 is supported for 1-D arrays only")
     if eb is None:
         eb = resolve_eb_device(config.error_bound, x)
-    if eb <= 0.0:
-        raise ConfigError(f"resolved error bound must be > 0, got {eb}")
+    check_resolved_eb(eb, x)
     x = x.contiguous()
     lib = _lib.load()
     g = _lib.geom(desc.dims, config.block_edge)
@@ -204,6 +233,16 @@ def decompress_device(codes: torch.Tensor, outliers: torch.Tensor, n_outliers: i
     g = _lib.geom(desc.dims, grid.block_edge)
     p = _lib.params(eb, radius, padding.kind_code, padding.gran_code)
     dev = codes.device
+    short = padding_shortfall(padding, grid, 0 if scalars is None else scalars.numel())
+    if short is not None:
+        # a padding section shorter than the policy needs (crafted container):
+        # the kernels never read past the caller's scalars, and the verdict is
+        # the reference's IndexError unless an earlier block fails first
+        need = padding.scalar_count(grid)
+        full = torch.zeros(need, dtype=torch.int64, device=dev)
+        if scalars is not None and scalars.numel():
+            full[: scalars.numel()] = scalars.reshape(-1)
+        scalars = full
     if out is None:
         out = torch.empty(desc.dims, dtype=torch.float32, device=dev)
     if result is None:
@@ -216,19 +255,37 @@ def decompress_device(codes: torch.Tensor, outliers: torch.Tensor, n_outliers: i
             ctypes.byref(p), _ptr(out), _ptr(result), _ptr(ws), ws.numel(), _stream(stream))
     if rc != 0:
         raise RuntimeError(f"vlz_dq_decompress failed ({rc})")
-    if check:
-        check_decompress(result, codes, counts, n_outliers, grid, radius)
+    if check or short is not None:
+        check_decompress(result, codes, counts, n_outliers, grid, radius, short)
     return out
 
 
-def check_decompress(result: torch.Tensor, codes, counts, n_outliers, grid, radius):
+def padding_shortfall(padding: PaddingPolicy, grid: BlockGrid, n_scalars: int):
+    """(first block, scalar index) at which the reference's halo lookup
+    (padding.py:113-129, apply_padding, run block by block in
+    reconstruct.py:104-124) indexes past a padding section of `n_scalars`
+    values, or None when the section is long enough."""
+    need = padding.scalar_count(grid)
+    if n_scalars >= need:
+        return None
+    if padding.granularity is PaddingGranularity.GLOBAL:
+        return 0, n_scalars
+    if padding.granularity is PaddingGranularity.BLOCK:
+        return n_scalars, n_scalars
+    return n_scalars // grid.descriptor.ndims, n_scalars  # edge: values[b*nd + d]
+
+
+def check_decompress(result: torch.Tensor, codes, counts, n_outliers, grid, radius, short=None):
     r = _lib.Result()
     buf = result.cpu().numpy()
     ctypes.memmove(ctypes.byref(r), buf.ctypes.data, 64)
+    if r.status == _lib.ST_SENTINEL_TOTAL:  # checked before the block loop
+        raise CorruptStreamError(f"{r.n_outliers} sentinel codes but {n_outliers} outliers")
+    if short is not None and (r.status == _lib.ST_OK or int(r.index) >= short[0]):
+        n = short[1]  # numpy's message for values[n] on a length-n array
+        raise IndexError(f"index {n} is out of bounds for axis 0 with size {n}")
     if r.status == _lib.ST_OK:
         return
-    if r.status == _lib.ST_SENTINEL_TOTAL:
-        raise CorruptStreamError(f"{r.n_outliers} sentinel codes but {n_outliers} outliers")
     bi = int(r.index)
     start, size = block_span(grid, bi)
     blk = codes[start:start + size].cpu().numpy()

@@ -8,7 +8,9 @@ Both run the dual-quant path on the GPU (libvlzgpu.so); the entropy stage
 (histogram on the GPU, canonical Huffman codebook + MSB-first coding natively
 on the host) and the container framing produce the reference's exact bytes.
 `lane_width` 1 and the vector lane widths give the same bytes, as in the
-reference (its scalar and vector kernels are byte-identical).
+reference (its scalar and vector kernels are byte-identical); lane width 1
+keeps the scalar kernel's error order (first offending index wins,
+kernel.py:138-145) where the vector path reports non-finite values first.
 """
 
 from __future__ import annotations
@@ -74,12 +76,11 @@ def _compress(data: np.ndarray, config: CompressionConfig, want_stream: bool):
     desc = ArrayDescriptor.from_array(data)
     eb = resolve_error_bound(config.error_bound, data)
     grid = build_block_grid(desc, config.block_edge)
-    if eb <= 0.0:
-        raise ConfigError(f"resolved error bound must be > 0, got {eb}")
+    gpu.check_resolved_eb(eb, data)
     x = _to_device(data, _device())
     dev = gpu.compress_device(x, config, eb=eb)
     try:
-        dev.check()
+        dev.check(scalar_order=config.lane_width == 1)  # pipeline.py:28-31
     except BoundTooSmallError as exc:
         raise BoundTooSmallError(exc.index, float(data.ravel()[exc.index]), eb) from None
     n_out = dev.n_outliers

@@ -153,11 +153,13 @@ def compress_sharded(x_local: torch.Tensor, full_shape, config: CompressionConfi
     backend = backend or GpuBackend()
     full = ArrayDescriptor(len(full_shape), tuple(int(d) for d in full_shape))
     full_grid = build_block_grid(full, config.block_edge)
+    # decided from the shape alone, so every rank raises together before any
+    # collective (a rank that went on would wait for the others forever)
+    if -(-full.dims[0] // config.block_edge) < world:
+        raise ConfigError("more ranks than dim-0 block layers")
     z0, z1 = slab_bounds(full.dims[0], config.block_edge, world, rank)
     if tuple(x_local.shape) != (z1 - z0,) + tuple(full.dims[1:]):
         raise ConfigError(f"rank {rank} holds {tuple(x_local.shape)}, expected planes [{z0},{z1})")
-    if z1 <= z0:
-        raise ConfigError("more ranks than dim-0 block layers")
     local = ArrayDescriptor(full.ndims, (z1 - z0,) + tuple(full.dims[1:]))
     local_grid = build_block_grid(local, config.block_edge)
     dev = x_local.device

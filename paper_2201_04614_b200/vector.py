@@ -85,20 +85,31 @@ def dualquant_vector(data: np.ndarray, config: CompressionConfig, collect_border
     return dualquant(data, config, collect_border)
 
 
-def dualquant(data: np.ndarray, config: CompressionConfig, collect_border: bool = False):
+def dualquant_scalar(data: np.ndarray, config: CompressionConfig, counters=None):
+    """Drop-in for the reference's scalar kernel (kernel.py:124-193): the
+    same stream as the vector path, and the scalar error order -- the first
+    flat index that is non-finite (ConfigError) or overflows the quantizer
+    (BoundTooSmallError) decides, kernel.py:138-145.  `counters` (the
+    reference's op tally for the paper's figures) is not supported."""
+    if counters is not None:
+        raise ConfigError("kernel counters are not collected by the GPU kernels")
+    return dualquant(data, config, scalar_order=True)
+
+
+def dualquant(data: np.ndarray, config: CompressionConfig, collect_border: bool = False,
+              scalar_order: bool = False):
     """dualquant_vector without the lane-width restriction (any lane width
     yields the same stream; used by pipeline.compress_detailed)."""
     desc = ArrayDescriptor.from_array(data)
     eb = resolve_error_bound(config.error_bound, data)
     build_block_grid(desc, config.block_edge)
-    if eb <= 0.0:
-        raise ConfigError(f"resolved error bound must be > 0, got {eb}")
+    gpu.check_resolved_eb(eb, data)
     dev = _device()
     x = torch.from_numpy(np.ascontiguousarray(data)).to(dev, non_blocking=False)
     out = gpu.compress_device(x, config, eb=eb)
     out.source = None
     try:
-        out.check()
+        out.check(scalar_order=scalar_order)
     except Exception as exc:
         from .errors import BoundTooSmallError
 

@@ -247,6 +247,33 @@ def make_errors():
     res = _exc(lambda: dualquant_vector(const, CompressionConfig(ErrorBound.relative(1e-3))))
     cases.append(dict(tag="degenerate_rel", data=const.tolist(), shape=[10], eb=None, rel=1e-3,
                       block_edge=16, padding="mean:global", expect=res))
+    # relative bounds over non-finite data: the resolved bound is NaN (or
+    # inf) and the non-finite scan names the index
+    for tag, vals in (("rel_nan", [1.0, 2.0, np.nan, 3.0]), ("rel_both_inf", [1.0, np.inf, -np.inf]),
+                      ("rel_inf", [1.0, 2.0, np.inf, 2.0])):
+        arr = np.array(vals, np.float32)
+        res = _exc(lambda: dualquant_vector(arr, CompressionConfig(ErrorBound.relative(1e-3))))
+        cases.append(dict(tag=tag, data=[float(v) for v in arr], shape=[arr.size], eb=None,
+                          rel=1e-3, block_edge=16, padding="mean:global", expect=res))
+    # lane width 1: compress() runs the scalar kernel, whose per-element
+    # check order differs from the vector path (kernel.py:138-145)
+    for tag, vals, eb in (("lane1_overflow_before_inf", [3e5, 1.0, np.inf, 2.0], 1e-5),
+                          ("lane1_nan_before_overflow", [1.0, np.nan, 3e5], 1e-5),
+                          ("lane1_overflow_2d", [[0.0, 1.0], [5e9, -np.inf]], 1.0),
+                          ("lane1_inf_first", [np.inf, 3e5], 1e-5),
+                          ("lane1_ok", [1.0, 2.0, 3.0], 1e-3)):
+        arr = np.array(vals, np.float32)
+        cfg = CompressionConfig(ErrorBound.absolute(eb), block_edge=8, lane_width=1,
+                                padding=PaddingPolicy.parse("mean:global"), radius=32768)
+        res = _exc(lambda: compress(arr, cfg))
+        cases.append(dict(tag=tag, data=arr.ravel().tolist(), shape=list(arr.shape), eb=eb,
+                          block_edge=8, padding="mean:global", lane=1, expect=res))
+    for tag, vals in (("lane1_rel_nan", [1.0, 3e5, np.nan]),):
+        arr = np.array(vals, np.float32)
+        cfg = CompressionConfig(ErrorBound.relative(1e-3), lane_width=1)
+        res = _exc(lambda: compress(arr, cfg))
+        cases.append(dict(tag=tag, data=arr.ravel().tolist(), shape=list(arr.shape), eb=None,
+                          rel=1e-3, block_edge=16, padding="mean:global", lane=1, expect=res))
     with open(os.path.join(HERE, "errors.json"), "w") as fh:
         json.dump(cases, fh, indent=1)
     print(f"wrote errors.json: {len(cases)} cases")
@@ -416,6 +443,117 @@ def make_container():
     with open(os.path.join(HERE, "container.json"), "w") as fh:
         json.dump(cases, fh)
     print(f"wrote container.json: {len(cases)} cases")
+
+
+def make_container_full():
+    """Reference decompress(blob) verdicts (any exception class, or the output
+    sha256) on crafted containers that pass the CRCs: over-subscribed
+    codebooks (Kraft sum > 1) and padding sections shorter than the policy
+    needs.  container_full.json."""
+    import struct
+    import zlib
+
+    H = struct.Struct("<4sHHBBBB3QddHHIQ5QI")
+
+    def rebuild(blob, new_sections):
+        """Re-lay the four sections with fresh offsets and both CRCs."""
+        f = list(H.unpack_from(blob, 0))
+        offs = [H.size]
+        for sec in new_sections[:-1]:
+            offs.append(offs[-1] + len(sec))
+        payload = b"".join(new_sections)
+        total = H.size + len(payload) + 4
+        f[16:20] = offs
+        f[20] = total
+        f[21] = 0
+        hdr = H.pack(*f)
+        f[21] = zlib.crc32(hdr)
+        return H.pack(*f) + payload + struct.pack("<I", zlib.crc32(payload))
+
+    def sections(blob):
+        f = H.unpack_from(blob, 0)
+        o = list(f[16:20]) + [len(blob) - 4]
+        return [blob[o[i]:o[i + 1]] for i in range(4)]
+
+    def verdict(blob):
+        try:
+            arr, _ = decompress(blob)
+        except Exception as exc:  # noqa: BLE001 -- any class the reference raises
+            return {"type": type(exc).__name__, "message": str(exc)}
+        return {"sha256": hashlib.sha256(np.ascontiguousarray(arr).tobytes()).hexdigest()}
+
+    rng = np.random.default_rng(91)
+    cases = []
+    srcs = []
+    d = _smooth(rng, (21, 17))
+    d[rng.random(d.shape) < 0.03] = 300.0
+    srcs.append(("mb2d", compress(d, _cfg(1e-4, 8, "mean:block", 512))))
+    d3 = _smooth(rng, (10, 12, 9))
+    srcs.append(("me3d", compress(d3, _cfg(1e-3, 8, "max:edge", 512))))
+    srcs.append(("mg3d", compress(d3, _cfg(1e-3, 8, "mean:global", 512))))
+    d1 = _smooth(rng, (300,))
+    srcs.append(("z1d", compress(d1, _cfg(1e-3, 16, "zero", 64))))
+    for name, blob in srcs:
+        pad, cb, codes, outl = sections(blob)
+        nsym = struct.unpack_from("<I", cb, 0)[0]
+        ent = [struct.unpack_from("<HB", cb, 4 + 3 * i) for i in range(nsym)]
+        nbits = struct.unpack_from("<Q", codes, 0)[0]
+        f = H.unpack_from(blob, 0)
+        count = f[15]
+
+        def book(lens):
+            return struct.pack("<I", len(lens)) + b"".join(
+                struct.pack("<HB", s, l) for (s, _), l in zip(ent, lens))
+
+        def with_nbits(nb):
+            return struct.pack("<Q", nb) + codes[8:]
+
+        muts = []
+        if nsym >= 3:
+            ones = [1] * nsym
+            muts.append(("all_len1", [pad, book(ones), codes, outl]))
+            # all length 1 and exactly `count` bits: decode succeeds with a
+            # two-symbol stream and the verdict comes from reconstruction
+            if count <= (len(codes) - 8) * 8:
+                muts.append(("all_len1_fit", [pad, book(ones), with_nbits(count), outl]))
+            short = [max(1, l - 1) for _, l in ent]
+            muts.append(("lens_minus1", [pad, book(short), codes, outl]))
+            three = [1, 1, 1] + [l for _, l in ent[3:]]
+            muts.append(("three_len1", [pad, book(three), codes, outl]))
+            longtail = [1] + [l for _, l in ent[1:-1]] + [40]
+            muts.append(("len1_long40", [pad, book(longtail), codes, outl]))
+        # padding section shorter / longer than the policy's scalar count
+        pc = struct.unpack_from("<Q", pad, 0)[0]
+        vals = pad[8:]
+        for k in sorted({0, 1, pc // 2, max(pc - 1, 0), pc + 3}):
+            if k == pc:
+                continue
+            body = (vals + b"\x07" * 8 * 8)[: 8 * k] if k > pc else vals[: 8 * k]
+            muts.append((f"padcount_{k}_of_{pc}", [struct.pack("<Q", k) + body, cb, codes, outl]))
+        # a corrupt block before / after the first short-padding block: the
+        # earlier failure wins (blocks run in order, reconstruct.py:120-122)
+        n_out, nz = struct.unpack_from("<QQ", outl, 0)
+        if nz >= 2 and pc >= 4:
+            pairs = [list(struct.unpack_from("<II", outl, 16 + 8 * i)) for i in range(nz)]
+            pairs[0][1] += 1
+            pairs[-1][1] -= 1
+            moved = outl[:16] + b"".join(struct.pack("<II", *q) for q in pairs) + outl[16 + 8 * nz:]
+            b0 = pairs[0][0]
+            nd = f[3]
+            per = 1 if name.startswith("mb") else nd
+            for k in (max(0, b0 * per - per), (b0 + 2) * per):
+                if k < pc:
+                    muts.append((f"partition_padcount_{k}",
+                                 [struct.pack("<Q", k) + vals[: 8 * k], cb, codes, moved]))
+            muts.append(("partition_only", [pad, cb, codes, moved]))
+        for tag, secs in muts:
+            m = rebuild(blob, secs)
+            cases.append(dict(tag=f"{name}_{tag}", blob=m.hex(), expect=verdict(m)))
+    with open(os.path.join(HERE, "container_full.json"), "w") as fh:
+        json.dump(cases, fh)
+    print(f"wrote container_full.json: {len(cases)} cases")
+    for c in cases:
+        print("  ", c["tag"], c["expect"])
 
 
 def _sha(a):

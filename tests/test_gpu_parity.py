@@ -89,22 +89,40 @@ def test_corpus_round_trip_matches_oracle(oracle, corpus_cases):
 
 
 def test_error_cases():
+    # vector-path cases go through dualquant_vector; lane-width-1 cases
+    # (scalar kernel order, kernel.py:138-145) through compress() at lane 1
+    # -- the reference's pipeline.py:28-31 dispatch -- and dualquant_scalar
+    import paper_2201_04614_b200 as vlzg
+    from paper_2201_04614_b200.vector import dualquant_scalar
+
+    n_lane1 = 0
     for c in load_json("errors.json"):
         data = np.array(c["data"], dtype=np.float32).reshape(c["shape"])
         exp = c["expect"]
+        lane = c.get("lane", 8)
         if c["eb"] is None:
-            cfg = M.CompressionConfig(M.ErrorBound.relative(c["rel"]), block_edge=c["block_edge"])
+            cfg = M.CompressionConfig(M.ErrorBound.relative(c["rel"]), block_edge=c["block_edge"],
+                                      lane_width=lane)
         else:
-            cfg = _cfg(c["eb"], c["block_edge"], c["padding"], 32768)
-        if exp is None:
-            dualquant_vector(data, cfg)
-            continue
-        cls = {"ConfigError": ConfigError, "BoundTooSmallError": BoundTooSmallError,
-               "DegenerateRangeError": DegenerateRangeError}[exp["type"]]
-        with pytest.raises(cls) as err:
-            dualquant_vector(data, cfg)
-        assert str(err.value) == exp["message"], c["tag"]
-        assert type(err.value) is cls
+            cfg = M.CompressionConfig(M.ErrorBound.absolute(c["eb"]), block_edge=c["block_edge"],
+                                      lane_width=lane, padding=M.PaddingPolicy.parse(c["padding"]),
+                                      radius=32768)
+        calls = [dualquant_vector] if lane != 1 else [vlzg.compress, dualquant_scalar]
+        n_lane1 += lane == 1
+        for fn in calls:
+            if exp is None:
+                fn(data, cfg)
+                continue
+            cls = {"ConfigError": ConfigError, "BoundTooSmallError": BoundTooSmallError,
+                   "DegenerateRangeError": DegenerateRangeError}[exp["type"]]
+            with pytest.raises(cls) as err:
+                fn(data, cfg)
+            assert str(err.value) == exp["message"], (c["tag"], fn.__name__)
+            assert type(err.value) is cls
+            if cls is BoundTooSmallError:
+                assert (err.value.index, err.value.value, err.value.bound) == (
+                    exp["index"], exp["value"], exp["bound"]), c["tag"]
+    assert n_lane1 >= 5
 
 
 def test_corrupt_streams(corrupt_cases):

@@ -98,3 +98,26 @@ def test_codestream_same_bytes():
     assert a.same_bytes(b)
     with pytest.raises(ConfigError):
         M.PaddingScalars(M.PaddingPolicy(), np.array([3], np.int32))
+
+
+def test_nan_relative_bound_names_first_nonfinite():
+    # a relative bound over NaN data resolves to NaN; the reference
+    # lets it past `eb <= 0` and reports the first non-finite index
+    from paper_2201_04614_b200.gpu import check_resolved_eb
+
+    n = 0
+    for c in load_json("errors.json"):
+        if not c["tag"].startswith("rel_"):
+            continue
+        data = np.array(c["data"], dtype=np.float32)
+        eb = M.resolve_error_bound(M.ErrorBound.relative(c["rel"]), data)
+        if eb == float("inf"):  # passes; the kernel's non-finite scan reports (GPU tests)
+            check_resolved_eb(eb, data)
+            continue
+        with pytest.raises(ConfigError) as err:
+            check_resolved_eb(eb, data)
+        assert str(err.value) == c["expect"]["message"], c["tag"]
+        n += 1
+    assert n == 1
+    with pytest.raises(ConfigError, match="must be > 0"):
+        check_resolved_eb(0.0, np.zeros(3, np.float32))

@@ -57,8 +57,8 @@ def test_oracle_error_cases(oracle):
     for c in load_json("errors.json"):
         data = np.array(c["data"], dtype=np.float32).reshape(c["shape"])
         exp = c["expect"]
-        if c["eb"] is None:
-            continue  # relative-bound resolution is host logic (tests/test_model.py)
+        if c["eb"] is None or c.get("lane", 8) == 1:
+            continue  # relative-bound resolution and the lane-1 order are host logic
         if exp is None:
             oracle.dualquant(data, c["eb"], c["block_edge"], 32768, c["padding"])
             continue

@@ -147,3 +147,47 @@ def test_slab_bounds_partition():
             assert z0 == prev and z0 % b == 0
             prev = z1
         assert prev == d0
+
+
+def _too_many_ranks_worker(rank, world, port, results):
+    sys.path[:0] = [REPO, os.path.join(REPO, "oracle")]
+    import oracle
+
+    from paper_2201_04614_b200 import model as M
+    from paper_2201_04614_b200.errors import ConfigError
+    from paper_2201_04614_b200.sharded import compress_sharded, slab_bounds
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        shape = (12, 9, 10)  # 2 block layers of b=8 for 3 ranks
+        z0, z1 = slab_bounds(shape[0], 8, world, rank)
+        data = _field(shape, 0)
+        cfg = M.CompressionConfig(M.ErrorBound.relative(1e-3), block_edge=8)
+        try:
+            compress_sharded(torch.from_numpy(np.ascontiguousarray(data[z0:z1])), shape, cfg,
+                             backend=OracleBackend(oracle))
+            results[rank] = "no error"
+        except ConfigError as exc:
+            results[rank] = str(exc)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_more_ranks_than_layers_raises_on_every_rank():
+    # only the empty-slab rank used to raise; the others entered
+    # the range all-reduce and waited forever
+    manager = mp.Manager()
+    results = manager.dict()
+    ctx = mp.spawn(_too_many_ranks_worker, args=(3, _free_port(), results), nprocs=3,
+                   join=False)
+    import time
+
+    deadline = time.time() + 120
+    while not ctx.join(timeout=5) and time.time() < deadline:
+        pass
+    alive = [p for p in ctx.processes if p.is_alive()]
+    for p in alive:
+        p.kill()
+    assert not alive, "a rank hung in a collective"
+    assert dict(results) == {r: "more ranks than dim-0 block layers" for r in range(3)}
