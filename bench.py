@@ -53,7 +53,14 @@ FALLBACK_HBM = 6650.0
 
 def parse():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--gpus", type=int, default=1,
+                    help="ranks (one per GPU); without torchrun's env, bench.py re-launches "
+                         "itself under torch.distributed.run with this many processes")
+    ap.add_argument("--spawn", action="store_true",
+                    help="re-launch under torch.distributed.run even for --gpus 1")
+    ap.add_argument("--cpu-check", action="store_true",
+                    help="host-logic dry run on CPU (gloo ranks, the CPU oracle per shard, "
+                         "small field): prints the stream digest; used by the tests")
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -64,6 +71,102 @@ def parse():
 
 
 # ------------------------------------------------------------------ helpers
+
+
+def free_port() -> int:
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def maybe_spawn(args) -> bool:
+    """`python bench.py --gpus N` without torchrun's environment: re-launch
+    this script as N ranks (one process per GPU) under torch.distributed.run
+    on 127.0.0.1 and return its exit code through sys.exit.  NCCL_DEBUG=INFO
+    (to stderr) so the communicator lines show the N ranks.  The reference
+    arm runs on one host process and never spawns."""
+    if "WORLD_SIZE" in os.environ or args.impl == "reference":
+        return False
+    if args.gpus <= 1 and not args.spawn:
+        return False
+    argv = [a for a in sys.argv[1:] if a != "--spawn"]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={free_port()}", os.path.abspath(__file__)] + argv
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    env.setdefault("OMP_NUM_THREADS", "1")
+    env["VLZ_BENCH_SPAWNED"] = "1"
+    print(f"[bench] spawning {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    sys.exit(subprocess.call(cmd, env=env))
+
+
+# Stream digest: the compressed stream is cut into DIGEST_PIECES equal
+# z-ranges (block aligned; every rank count dividing it owns whole pieces),
+# each piece hashed as sha256(sha256(codes) | sha256(counts) | sha256(outlier
+# values)), and the digest is sha256 over the piece hashes in order plus the
+# padding scalars.  It is therefore the same for 1, 2, 4 and 8 ranks exactly
+# when the concatenated stream is byte-identical to the 1-GPU stream.
+DIGEST_PIECES = 8
+# digest of the default C5 stream (2048 planes), recorded from a 1-GPU run
+C5_STREAM_DIGEST = None
+
+
+def piece_hashes(codes_u16, counts_i64, outliers_f32, z0, z1, D0, plane, per_layer, block):
+    """[(piece, sha256 digest bytes)] for the pieces inside planes [z0, z1) of
+    a D0-plane field; the arrays hold this rank's slab (host numpy, or CUDA
+    tensors copied piece by piece).  Threads hash the pieces in parallel
+    (hashlib releases the GIL)."""
+    import hashlib
+    from concurrent.futures import ThreadPoolExecutor
+
+    P = D0 // DIGEST_PIECES
+    assert P % block == 0 and z0 % P == 0 and z1 % P == 0, "pieces must tile the slab"
+
+    def host(a, lo, hi):
+        v = a[lo:hi]
+        return v.cpu().numpy() if hasattr(v, "cpu") else v
+
+    # exclusive outlier offsets at the piece boundaries (local block index)
+    bounds = [(k, (k * P - z0) // block * per_layer) for k in range(z0 // P, z1 // P + 1)]
+    if hasattr(counts_i64, "cpu"):
+        import torch
+
+        cs = torch.cumsum(counts_i64, 0)
+        offs = [0 if b == 0 else int(cs[b - 1].item()) for _, b in bounds]
+    else:
+        cs = np.cumsum(counts_i64)
+        offs = [0 if b == 0 else int(cs[b - 1]) for _, b in bounds]
+
+    def one(i):
+        k, b0 = bounds[i]
+        b1 = bounds[i + 1][1]
+        c0, c1 = (k * P - z0) * plane, ((k + 1) * P - z0) * plane
+        parts = (host(codes_u16, c0, c1), host(counts_i64, b0, b1),
+                 host(outliers_f32, offs[i], offs[i + 1]))
+        h = hashlib.sha256()
+        for a in parts:
+            h.update(hashlib.sha256(np.ascontiguousarray(a).tobytes()).digest())
+        return k, h.digest()
+
+    with ThreadPoolExecutor(max_workers=min(8, len(bounds) - 1)) as pool:
+        return list(pool.map(one, range(len(bounds) - 1)))
+
+
+def combine_digest(all_pieces, scalars_i64) -> str:
+    import hashlib
+
+    pieces = sorted(p for lst in all_pieces for p in lst)
+    assert [k for k, _ in pieces] == list(range(DIGEST_PIECES)), "pieces missing"
+    h = hashlib.sha256()
+    for _, d in pieces:
+        h.update(d)
+    h.update(np.ascontiguousarray(scalars_i64, dtype=np.int64).tobytes())
+    return h.hexdigest()
+
 
 
 def dist_env():
@@ -151,28 +254,36 @@ def oracle_round_trip(sample: np.ndarray, eb: float, threads: int):
 CPU_PLANES = 8  # bounded CPU sample: 8 x 2048 x 1024 = 16.8M elements (67 MB)
 
 
-def run_reference(args):
-    ws, rank, local = dist_env()
-    if rank != 0:
-        return  # the reference arm runs on rank 0 only
+def cpu_leg(steps: int, warmup: int):
+    """The CPU baseline, timed the same way in both arms: the CPU oracle's
+    compress + decompress round trip of the first CPU_PLANES planes of the C5
+    field (numpy build of the recipe, the full field's eb), on every host
+    core; median over `steps` timed runs after `warmup` untimed ones.
+    Returns (GB/s, median seconds, threads, sample description)."""
     from paper_2201_04614_b200 import workloads
 
     threads = os.cpu_count() or 1
     sample = workloads.gen_c5_slab_numpy((0, CPU_PLANES))
-    eb = C5_EB  # the full field's bound, the same one the GPU arm quantises with
-    for _ in range(args.warmup):
-        oracle_round_trip(sample, eb, threads)
-    times = [oracle_round_trip(sample, eb, threads) for _ in range(args.steps)]
-    tot = sum(times)
-    value = 4.0 * sample.size * args.steps / tot / 1e9
-    desc = (f"C5 slab {sample.shape[0]}x{SHAPE[1]}x{SHAPE[2]} ({sample.size} elements) "
-            f"compress+decompress round trip per step, eb of the full field")
+    for _ in range(warmup):
+        oracle_round_trip(sample, C5_EB, threads)
+    ts = [oracle_round_trip(sample, C5_EB, threads) for _ in range(max(1, steps))]
+    med = statistics.median(ts)
+    desc = (f"C5 slab {sample.shape[0]}x{SHAPE[1]}x{SHAPE[2]} ({sample.size} elements), CPU oracle "
+            f"compress+decompress round trip at the full field's eb, median of {len(ts)}")
+    return 4.0 * sample.size / med / 1e9, med, threads, desc
+
+
+def run_reference(args):
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return  # the reference arm runs on rank 0 only
+    value, med, threads, desc = cpu_leg(args.steps, args.warmup)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": 1e3 * med, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64+int64", "data": "synthetic (C5 recipe, numpy float64)",
-        "config": workload_config(args.gpus, eb),
+        "config": workload_config(args.gpus, C5_EB),
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "port",
                          "sample": desc},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -186,6 +297,56 @@ def workload_config(n, eb):
             "shape": list(SHAPE), "block_edge": BLOCK, "radius": RADIUS, "padding": PADDING,
             "eb_rel": REL_EB, "eb": eb, "parallelism": f"z-slab x{n}",
             "l2": "no flush: 17.2 GB input per step > 126 MB L2"}
+
+
+def run_cpu_check(args):
+    """The GPU arm's multi-rank orchestration on CPU: gloo ranks, value
+    range all-reduce, mean:global statistics all-gather (sharded.reduce_stats),
+    the pinned CPU oracle as each shard's compressor, piece hashes gathered on
+    rank 0 into the stream digest.  tests/test_bench_cpu.py runs it at 1 and 2
+    ranks and requires the same digest (and the single-process oracle's)."""
+    import torch
+    import torch.distributed as dist
+
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import oracle
+
+    from paper_2201_04614_b200 import workloads
+    from paper_2201_04614_b200.sharded import reduce_stats
+
+    ws, rank, _ = dist_env()
+    if ws > 1:
+        dist.init_process_group("gloo")
+    shape = (args.planes if args.planes != SHAPE[0] else 64, 48, 40)
+    D0 = shape[0]
+    assert D0 % (BLOCK * ws) == 0 and DIGEST_PIECES % ws == 0
+    per = D0 // ws
+    z0, z1 = rank * per, (rank + 1) * per
+    x = workloads.gen_c5_slab_numpy((z0, z1), shape=shape)
+    lo, hi = oracle.minmax(x)
+    mm = torch.tensor([lo, -hi], dtype=torch.float64)
+    if ws > 1:
+        dist.all_reduce(mm, op=dist.ReduceOp.MIN)
+    eb = REL_EB * (-float(mm[1]) - float(mm[0]))
+    st = oracle.global_stats(x, eb)
+    stats = torch.tensor([st[0], st[1], st[2], -st[3]], dtype=torch.int64)
+    if ws > 1:
+        reduce_stats(stats)
+    s0 = oracle.stat_value("mean", int(stats[0]), int(stats[1]), int(stats[2]), -int(stats[3]))
+    o = oracle.dualquant(x, eb, BLOCK, RADIUS, PADDING, threads=1, global_scalar=s0)
+    per_layer = -(-shape[1] // BLOCK) * -(-shape[2] // BLOCK)
+    mine = piece_hashes(o["codes"].astype(np.uint16), o["outlier_counts"], o["outlier_values"],
+                        z0, z1, D0, shape[1] * shape[2], per_layer, BLOCK)
+    if ws > 1:
+        allp = [None] * ws
+        dist.all_gather_object(allp, mine)
+    else:
+        allp = [mine]
+    if rank == 0:
+        print(json.dumps({"cpu_check": True, "n_ranks": ws, "shape": list(shape), "eb": eb,
+                          "scalar": s0, "stream_digest": combine_digest(allp, [s0])}), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
 
 
 # ------------------------------------------------------------------ GPU arm
@@ -358,26 +519,41 @@ def run_ours(args):
     achieved = alg / (kt * 1e-3) / 1e9 if kt > 0 else 0.0  # (VLZ_BENCH_KTIMING=0: no kernel times)
     traffic = load_traffic(dom)
 
+    # stream digest (outside the timed region): the same for every rank count
+    digest = None
+    if DIGEST_PIECES % ws == 0 and D0 % (DIGEST_PIECES * BLOCK) == 0:
+        per_layer = grid.blocks_per_dim[1] * grid.blocks_per_dim[2]
+        mine = piece_hashes(codes, counts, outl, z0, z1, D0, SHAPE[1] * SHAPE[2], per_layer, BLOCK)
+        allp = [None] * ws
+        if ws > 1:
+            dist.all_gather_object(allp, mine)
+        else:
+            allp = [mine]
+        if rank == 0:
+            digest = combine_digest(allp, scalars.cpu().numpy())
+    if rank == 0 and digest is not None and D0 == SHAPE[0] and C5_STREAM_DIGEST is not None:
+        assert digest == C5_STREAM_DIGEST, f"stream digest {digest} != 1-GPU {C5_STREAM_DIGEST}"
+
     e2e = None
     if not args.no_e2e:
         e2e = measure_e2e(args, x, eb, cfg, ws, rank, dev)
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        threads = os.cpu_count() or 1
-        sample = x[:CPU_PLANES].cpu().numpy()
-        oracle_round_trip(sample, eb, threads)
-        ts = [oracle_round_trip(sample, eb, threads) for _ in range(3)]
-        cpu = {"value": 4.0 * sample.size / statistics.median(ts) / 1e9, "unit": "GB/s",
-               "cores": threads, "kind": "port",
-               "sample": f"C5 slab {sample.shape[0]}x{SHAPE[1]}x{SHAPE[2]} ({sample.size} elements),"
-                         f" CPU oracle compress+decompress, median of 3"}
+        v, _, threads, desc = cpu_leg(3, 1)
+        cpu = {"value": v, "unit": "GB/s", "cores": threads, "kind": "port", "sample": desc}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws, "steps": K,
             "warmup": args.warmup, "ms_per_step": elapsed / K, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64+int32",
             "data": "synthetic (C5 recipe: 64 seeded 3D sinusoidal modes + N(0,1e-3), on device)",
-            "config": dict(workload_config(ws, eb), eb_matches_reference_arm=(eb == C5_EB)),
+            "config": workload_config(ws, eb),
+            "eb_matches_reference_arm": eb == C5_EB,
+            "stream_digest": digest,
+            "stream_digest_matches_1gpu": (None if C5_STREAM_DIGEST is None or D0 != SHAPE[0]
+                                           else digest == C5_STREAM_DIGEST),
+            "nccl": ({"backend": dist.get_backend(), "world": ws,
+                      "spawned": os.environ.get("VLZ_BENCH_SPAWNED") == "1"} if ws > 1 else None),
             "compress_gbs": in_bytes / (tc / K * 1e-3) / 1e9,
             "decompress_gbs": in_bytes / (td / K * 1e-3) / 1e9,
             "kernel_ms_per_step": {"fused_compress": k1 / K, "fused_decompress": k4 / K,
@@ -551,7 +727,10 @@ def measure_e2e(args, x, eb, cfg, ws, rank, dev):
 
 def main():
     args = parse()
-    if args.impl == "reference":
+    maybe_spawn(args)
+    if args.cpu_check:
+        run_cpu_check(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

@@ -111,6 +111,8 @@ def value_range_eb(data: np.ndarray, rel: float) -> float:
     return float(rel) * (float(data.max()) - float(data.min()))
 
 
+NOISE_GROUP = 8  # planes per noise seed in the C5 generators (one b=8 block layer)
+
 # --------------------------------------------------------------------------
 # device-side generators (bench only; no parity pin needed, these just have
 # to be the same field on every run)
@@ -141,12 +143,16 @@ def gen_modes_torch(shape, count, kmax, power, noise, seed, device, z_range=None
         ca = (float(amp[m]) * torch.cos(a)).float()
         out.addcmul_(sa[:, None, None], cb[None])
         out.addcmul_(ca[:, None, None], sb[None])
+    # noise per group of NOISE_GROUP planes, each from its own seed: any
+    # block-aligned slab of the field is the same slice of the whole field
+    # (z-sharded runs then see exactly the 1-GPU field)
     gen = torch.Generator(device=device)
-    gen.manual_seed(seed * 1_000_003 + z0)
-    step = max(1, (1 << 28) // (D1 * D2))
-    for p in range(0, z1 - z0, step):
-        sl = out[p:p + step]
-        sl.add_(torch.randn(sl.shape, generator=gen, device=device, dtype=torch.float32), alpha=noise)
+    for g0 in range(z0 - z0 % NOISE_GROUP, z1, NOISE_GROUP):
+        gen.manual_seed(seed * 1_000_003 + g0 // NOISE_GROUP)
+        nz = torch.randn((NOISE_GROUP, D1, D2), generator=gen, device=device,
+                         dtype=torch.float32)
+        a, b = max(g0, z0), min(g0 + NOISE_GROUP, z1)
+        out[a - z0:b - z0].add_(nz[a - g0:b - g0], alpha=noise)
     return out
 
 
@@ -179,5 +185,9 @@ def gen_c5_slab_numpy(z_range, shape=(2048, 2048, 1024), seed: int = 5) -> np.nd
             np.multiply(im, ca[p], out=t2)
             acc[p] += t2
     out = acc.astype(np.float32)
-    out += np.random.default_rng(seed * 1_000_003 + z0).normal(0.0, 1e-3, out.shape).astype(np.float32)
+    for g0 in range(z0 - z0 % NOISE_GROUP, z1, NOISE_GROUP):  # as gen_modes_torch
+        nz = np.random.default_rng(seed * 1_000_003 + g0 // NOISE_GROUP).normal(
+            0.0, 1e-3, (NOISE_GROUP, D1, D2)).astype(np.float32)
+        a, b = max(g0, z0), min(g0 + NOISE_GROUP, z1)
+        out[a - z0:b - z0] += nz[a - g0:b - g0]
     return out
