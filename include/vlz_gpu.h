@@ -243,6 +243,18 @@ int vlz_timing_collect(double* ms, int64_t* launches, int n);
 /* library build string (arch, commit) */
 const char* vlz_version(void);
 
+/* ---- test support (not on any product path; tests/test_gpu_sweep.py) ---- *
+ * Exhaustive check of the float32 exact-fast prequantizer against the exact
+ * float64 one (quantize.py:31-42,66-78; vector.py:72-77) over all 2^32 float
+ * bit patterns at bound eb.  d_counts (device uint64[6]) receives: accepted
+ * by the fast path, finite but sent to the exact path, non-finite, accepted
+ * but wrong (n differs, overflow or narrowing failure -- must be 0), scalar
+ * vs paired-FP32 form disagreements (must be 0), first offending pattern
+ * (UINT64_MAX when none).  Stream-ordered. */
+int vlz_test_prequant_sweep(double eb, unsigned long long* d_counts, void* stream);
+/* 1 when the fast path is enabled for this eb (1/(2eb) in (2^-100, 2^100)) */
+int vlz_test_fast_enabled(double eb);
+
 #ifdef __cplusplus
 }
 #endif

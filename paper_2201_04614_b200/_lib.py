@@ -86,6 +86,8 @@ PROTOTYPES = {
     "vlz_timing": (None, [ctypes.c_int]),
     "vlz_timing_collect": (ctypes.c_int, [_P(ctypes.c_double), _P(_i64), ctypes.c_int]),
     "vlz_version": (ctypes.c_char_p, []),
+    "vlz_test_prequant_sweep": (ctypes.c_int, [ctypes.c_double, _vp, _vp]),
+    "vlz_test_fast_enabled": (ctypes.c_int, [ctypes.c_double]),
 }
 
 _lib = None

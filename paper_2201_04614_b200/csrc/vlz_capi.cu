@@ -266,20 +266,6 @@ int to_rc(cudaError_t e) {
   return VLZ_E_CUDA;
 }
 
-QP make_qp(const vlz_params* p) {
-  QP q;
-  q.eb = p->eb;
-  q.twoeb = 2.0 * p->eb;
-  q.radius = p->radius;
-  q.kind = p->pad_kind;
-  // float32 fast path only where 1/(2eb) is a normal float with margin
-  const double inv = 1.0 / q.twoeb;
-  const bool fast_ok = q.twoeb > 0.0 && inv > 0x1p-100 && inv < 0x1p100;
-  q.inv32 = fast_ok ? (float)inv : 0.0f;
-  q.lim0 = fast_ok ? (float)(0.5 - 0x1p-22) : -1.0f;
-  q.kq = (float)0x1p-21;
-  return q;
-}
 
 // ---- value range (ErrorBound.relative) -------------------------------
 __device__ __forceinline__ unsigned fkey(float f) {
@@ -341,6 +327,23 @@ __global__ void minmax_init(unsigned int* w) {
 }
 
 }  // namespace
+
+// shared with the test-support sweep (k_sweep.cu)
+QP make_qp(const vlz_params* p) {
+  QP q;
+  q.eb = p->eb;
+  q.twoeb = 2.0 * p->eb;
+  q.radius = p->radius;
+  q.kind = p->pad_kind;
+  // float32 fast path only where 1/(2eb) is a normal float with margin
+  const double inv = 1.0 / q.twoeb;
+  const bool fast_ok = q.twoeb > 0.0 && inv > 0x1p-100 && inv < 0x1p100;
+  q.inv32 = fast_ok ? (float)inv : 0.0f;
+  q.lim0 = fast_ok ? (float)(0.5 - 0x1p-22) : -1.0f;
+  q.kq = (float)0x1p-21;
+  return q;
+}
+
 }  // namespace vlz
 
 using namespace vlz;

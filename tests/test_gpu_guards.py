@@ -52,12 +52,52 @@ SHAPES = [((1000,), 64), ((777,), 8), ((24, 40), 8), ((37, 70), 16), ((16, 16, 2
 @pytest.mark.parametrize("shape,b", SHAPES)
 @pytest.mark.parametrize("pol", ["zero", "mean:global", "max:block", "min:edge"])
 def test_no_out_of_bounds_writes(shape, b, pol):
-    lib = _lib.load()
     rng = np.random.default_rng(len(shape) * 100 + b)
     idx = np.indices(shape).astype(np.float64)
     data = sum(np.sin(0.1 * (k + 1) * idx[k]) * 30 for k in range(len(shape)))
     data = (data + rng.normal(0, 0.3, shape)).astype(np.float32)
-    eb, radius = 1e-2, 64
+    _run_guarded(data, b, pol, 1e-2, 64)
+
+
+def _field(kind, shape, seed):
+    rng = np.random.default_rng(seed)
+    if kind == "walk":  # 1-D random walk with spikes (fused 1-D kernels)
+        d = np.cumsum(rng.normal(0, 1, shape)) * 0.01
+        d[rng.random(shape) < 0.01] = 50.0
+        return d.astype(np.float32)
+    if kind == "huge":  # |d| >= 2^24: the int64 redo tiles
+        return (rng.uniform(-1, 1, shape) * 1.0e9).astype(np.float32)
+    idx = np.indices(shape).astype(np.float64)
+    d = sum(np.sin(0.05 * (k + 1) * idx[k]) for k in range(len(shape))) * 10
+    return (d + rng.normal(0, 0.05, shape)).astype(np.float32)
+
+
+# paths the small shapes above do not reach (round 2): the fused 1-D kernels
+# (bulk-copy ring, >= 4 M elements), 8-row staged b = 32 / 64 fast kernels,
+# outlier-heavy blocks (eb 1e-4 at radius 64) and the int64 redo list
+LARGE = [
+    ("walk", (1 << 22,), 256, "zero", 1e-3, 512),
+    ("walk", (1 << 22,) , 64, "mean:global", 1e-3, 512),
+    ("waves", (64, 64, 128), 64, "mean:block", 1e-4, 64),
+    ("waves", (32, 64, 128), 32, "max:edge", 1e-2, 64),
+    ("waves", (64, 256), 64, "mean:global", 1e-4, 64),
+    ("huge", (40, 33, 70), 8, "mean:global", 1.0, 512),
+    ("huge", (24, 40, 64), 16, "zero", 1.0, 512),
+]
+
+
+@pytest.mark.parametrize("kind,shape,b,pol,eb,radius", LARGE)
+def test_no_out_of_bounds_writes_large_paths(kind, shape, b, pol, eb, radius):
+    M.allow_block_256(True)
+    try:
+        _run_guarded(_field(kind, shape, b), b, pol, eb, radius)
+    finally:
+        M.allow_block_256(False)
+
+
+def _run_guarded(data, b, pol, eb, radius):
+    lib = _lib.load()
+    shape = data.shape
     n = data.size
     grid = M.build_block_grid(M.ArrayDescriptor(len(shape), shape), b)
     policy = M.PaddingPolicy.parse(pol)
@@ -130,3 +170,40 @@ def test_no_out_of_bounds_writes(shape, b, pol):
     for name, gbuf in (("decoded", dec), ("workspace", dws), ("payload", dpay)):
         gbuf.check(f"decode {name}")
     assert torch.equal(dec.view(torch.int16), c16)
+
+
+def test_crafted_books_device_decode_guards():
+    """Over-subscribed codebooks from crafted containers: the
+    device decoder's table builder and decode passes stay inside their
+    buffers (the verdicts themselves are pinned in test_container_full)."""
+    from conftest import load_json
+    from paper_2201_04614_b200.container import deserialize
+
+    lib = _lib.load()
+    n_books = 0
+    for c in load_json("container_full.json"):
+        p = deserialize(bytes.fromhex(c["blob"]))
+        cb = p.codebook
+        if not len(cb.lengths) or int(cb.lengths.max()) > 58:
+            continue
+        pay = bytes(p.code_bits)
+        nbytes = len(pay)
+        count = p.descriptor.element_count
+        dpay = Guarded((nbytes + 3) // 4 * 4 + 16, fill=0)
+        if nbytes:
+            dpay.view(torch.uint8)[:nbytes].copy_(torch.frombuffer(bytearray(pay),
+                                                                   dtype=torch.uint8).cuda())
+        dec = Guarded(2 * count)
+        dws = Guarded(int(lib.vlz_huff_decode_ws_size(nbytes)), fill=0)
+        syms = np.ascontiguousarray(cb.symbols, dtype=np.uint16)
+        lens = np.ascontiguousarray(cb.lengths, dtype=np.uint8)
+        consumed = ctypes.c_int64(0)
+        rc = lib.vlz_huff_decode_device(dpay.ptr(), nbytes, p.code_bit_length, syms.ctypes.data,
+                                        lens.ctypes.data, len(syms), count, dec.ptr(),
+                                        ctypes.byref(consumed), dws.ptr(), dws.n, None)
+        assert rc >= 0, c["tag"]
+        torch.cuda.synchronize()
+        for name, gbuf in (("decoded", dec), ("workspace", dws), ("payload", dpay)):
+            gbuf.check(f"{c['tag']} decode {name}")
+        n_books += 1
+    assert n_books >= 20
