@@ -55,6 +55,24 @@ size_t chunk_bytes() {
   return v;
 }
 
+// Chunks whose host->device copy may be queued ahead of the one completing
+// (VLZ_INFLIGHT overrides; 0 = no limit).  With the copy streams shared by
+// all calls of a device (below), a call that queued its whole array at once
+// would hold off every copy a concurrent call makes in that direction; a
+// window of two lets a compress (mostly H2D) and a decompress (mostly D2H)
+// interleave chunk by chunk on the full-duplex link.  Measured on a B200
+// (8.6 GB field, tools/e2e_probe.py, profiles/r02/e2e_probe.txt): compress ||
+// decompress 297 ms with shared streams and a window of 2, 321 ms with
+// shared streams unthrottled, ~346 ms with per-call streams (no overlap: the
+// pair took as long as the two calls in sequence).
+size_t inflight() {
+  static const size_t v = [] {
+    const char* e = std::getenv("VLZ_INFLIGHT");
+    return size_t(e ? std::atol(e) : 2);
+  }();
+  return v;
+}
+
 size_t a256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Chunk {
@@ -103,7 +121,23 @@ struct Ctx {
   void* hbuf = nullptr;
   size_t hcap = 0;
   bool busy = false;
+  cudaEvent_t fence[2] = {nullptr, nullptr};  // this call's position on a copy stream
 };
+
+// Every context of a device queues its copies on one host->device and one
+// device->host stream shared by all concurrent calls (VLZ_SHARED_COPY=0: a
+// stream pair per context), so the two directions map onto two copy queues
+// as in a plain duplex copy; per-context streams left concurrent calls
+// serialised on the link.
+bool shared_copy() {
+  static const bool v = [] {
+    const char* e = std::getenv("VLZ_SHARED_COPY");
+    return !e || std::atoi(e) != 0;
+  }();
+  return v;
+}
+cudaStream_t g_copy[64][2];
+std::mutex g_copy_mu;
 // Per device, a small pool of contexts (streams + device buffer): concurrent
 // calls from different host threads each take their own context, so e.g. a
 // compress (mostly host->device traffic) and a decompress (mostly
@@ -142,11 +176,14 @@ struct Lease {
   }
   ~Lease() {
     // nothing of this call may still be in flight when the context is reused
-    // (early error returns leave copies queued)
+    // (early error returns leave copies queued); the copy streams may be
+    // shared, so wait for this call's last copy rather than the stream
     if (cx->h2d) {
-      cudaStreamSynchronize(cx->h2d);
+      cudaEventRecord(cx->fence[0], cx->h2d);
+      cudaEventRecord(cx->fence[1], cx->d2h);
+      cudaEventSynchronize(cx->fence[0]);
+      cudaEventSynchronize(cx->fence[1]);
       cudaStreamSynchronize(cx->comp);
-      cudaStreamSynchronize(cx->d2h);
     }
     cudaSetDevice(prev);
     release(cx);
@@ -155,9 +192,23 @@ struct Lease {
 
 bool ensure(Ctx& c, size_t need, size_t nev, size_t hneed) {
   if (!c.h2d) {
-    cudaStreamCreateWithFlags(&c.h2d, cudaStreamNonBlocking);
     cudaStreamCreateWithFlags(&c.comp, cudaStreamNonBlocking);
-    cudaStreamCreateWithFlags(&c.d2h, cudaStreamNonBlocking);
+    if (shared_copy()) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      std::lock_guard<std::mutex> lk(g_copy_mu);
+      if (!g_copy[dev][0]) {
+        cudaStreamCreateWithFlags(&g_copy[dev][0], cudaStreamNonBlocking);
+        cudaStreamCreateWithFlags(&g_copy[dev][1], cudaStreamNonBlocking);
+      }
+      c.h2d = g_copy[dev][0];
+      c.d2h = g_copy[dev][1];
+    } else {
+      cudaStreamCreateWithFlags(&c.h2d, cudaStreamNonBlocking);
+      cudaStreamCreateWithFlags(&c.d2h, cudaStreamNonBlocking);
+    }
+    cudaEventCreateWithFlags(&c.fence[0], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&c.fence[1], cudaEventDisableTiming);
   }
   if (c.cap < need) {
     if (c.buf) cudaFree(c.buf);
@@ -187,6 +238,12 @@ int64_t scalars_at(const vlz_params* p, int nd, int64_t block_off) {
 }
 
 int rc_of(cudaError_t e) { return e == cudaSuccess ? VLZ_OK : VLZ_E_CUDA; }
+
+// wait for everything this call queued on device->host copy stream so far
+cudaError_t d2h_fence(Ctx& c) {
+  cudaEventRecord(c.fence[1], c.d2h);
+  return cudaEventSynchronize(c.fence[1]);
+}
 
 // VLZ_HOST_PROFILE=1: phase times of the host entry points on stderr
 bool host_profile() {
@@ -257,8 +314,10 @@ int vlz_dq_compress_host(const float* h_in, const vlz_geom* gg, const vlz_params
     ws_off[i] = wo;
     wo += a256(ch[i].ws_bytes);
   }
+  const size_t win = inflight();
   for (size_t i = 0; i < nc && rc == VLZ_OK; ++i) {
     const Chunk& c = ch[i];
+    if (win && i >= win) cudaEventSynchronize(cx.ev[2 * (i - win)]);
     cudaMemcpyAsync(d_in + c.elem_off, h_in + c.elem_off, c.n * 4, cudaMemcpyHostToDevice, cx.h2d);
     cudaEventRecord(cx.ev[2 * i], cx.h2d);
     cudaStreamWaitEvent(cx.comp, cx.ev[2 * i], 0);
@@ -310,7 +369,7 @@ int vlz_dq_compress_host(const float* h_in, const vlz_geom* gg, const vlz_params
     if (ns > 0) cudaMemcpyAsync(h_scalars, d_sc, ns * 8, cudaMemcpyDeviceToHost, cx.d2h);
     cudaMemcpyAsync(res, d_res, 64 * nc, cudaMemcpyDeviceToHost, cx.d2h);
     cudaMemcpyAsync(npatch, d_pc, 4 * nc, cudaMemcpyDeviceToHost, cx.d2h);
-    rc = rc_of(cudaStreamSynchronize(cx.d2h));
+    rc = rc_of(d2h_fence(cx));
     // combine: first non-finite index anywhere, else first overflow index
     vlz_result out{};
     int64_t nf = INT64_MAX, ov = INT64_MAX, nout = 0;
@@ -350,7 +409,7 @@ int vlz_dq_compress_host(const float* h_in, const vlz_geom* gg, const vlz_params
         if (npatch[i])
           cudaMemcpyAsync(patches + pstart[i], d_pl + ch[i].block_off, 8ull * npatch[i],
                           cudaMemcpyDeviceToHost, cx.d2h);
-      rc = rc_of(cudaStreamSynchronize(cx.d2h));
+      rc = rc_of(d2h_fence(cx));
       const auto tp = std::chrono::steady_clock::now();
       // chunks patch disjoint code ranges: spread them over a few host threads
       auto apply = [&](size_t i0, size_t i1) {
@@ -425,8 +484,10 @@ int vlz_dq_decompress_host(const uint16_t* h_codes, const float* h_outliers, int
   if (ns > 0) cudaMemcpyAsync(d_sc, h_scalars, ns * 8, cudaMemcpyHostToDevice, cx.h2d);
   size_t wo = o_ws;
   int rc = VLZ_OK;
+  const size_t win = inflight();
   for (size_t i = 0; i < nc && rc == VLZ_OK; ++i) {
     const Chunk& c = ch[i];
+    if (win && i >= win) cudaEventSynchronize(cx.ev[2 * (i - win)]);
     cudaMemcpyAsync(d_codes + c.elem_off, h_codes + c.elem_off, c.n * 2, cudaMemcpyHostToDevice,
                     cx.h2d);
     const int64_t no = ooff[i + 1] - ooff[i];
@@ -448,7 +509,7 @@ int vlz_dq_decompress_host(const uint16_t* h_codes, const float* h_outliers, int
     cudaEventRecord(cx.ev[2 * nc], cx.comp);
     cudaStreamWaitEvent(cx.d2h, cx.ev[2 * nc], 0);
     cudaMemcpyAsync(res, d_res, 64 * nc, cudaMemcpyDeviceToHost, cx.d2h);
-    rc = rc_of(cudaStreamSynchronize(cx.d2h));
+    rc = rc_of(d2h_fence(cx));
   }
   if (rc == VLZ_OK) {
     vlz_result out{};

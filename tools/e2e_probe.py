@@ -13,7 +13,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2201_04614_b200 import _lib  # noqa: E402
 from paper_2201_04614_b200 import model as M  # noqa: E402
 
-shape = (256, 2048, 1024)
+shape = (int(sys.argv[1]) if len(sys.argv) > 1 else 256, 2048, 1024)
+K = int(sys.argv[2]) if len(sys.argv) > 2 else 6
 n = int(np.prod(shape))
 x = torch.linspace(0, 50, n, device="cuda").sin_().reshape(shape)
 h_in = torch.empty(shape, dtype=torch.float32, pin_memory=True)
@@ -50,7 +51,6 @@ comp(bufs[0])
 comp(bufs[1])
 decomp(bufs[0])
 decomp(bufs[1])
-K = 6
 
 
 def loop(fn, b):
@@ -68,4 +68,5 @@ for name, jobs in [("compress alone", [(comp, bufs[0])]), ("decompress alone", [
     for x_ in th:
         x_.join()
     dt = (time.perf_counter() - t) / K
-    print(f"{name:26s} {dt * 1e3:7.1f} ms per iteration ({len(jobs)} calls)")
+    print(f"{shape[0]} planes chunk {os.environ.get('VLZ_CHUNK_MB', '64')} MB: {name:26s} "
+          f"{dt * 1e3:7.1f} ms per iteration ({len(jobs)} calls)", flush=True)
