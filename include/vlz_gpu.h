@@ -231,6 +231,16 @@ int vlz_huff_decode(const uint8_t* h_payload, int64_t nbytes, int64_t bit_length
 int vlz_border_outliers(const uint16_t* d_codes, const vlz_geom* g, int64_t* d_total,
                         void* stream);
 
+/* padding-policy census for outlier_report (padding.py:162-205): for every
+ * policy, the block origins that are outliers (|d_o - s0| > R-1 or a failed
+ * narrowing check; by finding 1 the only elements whose verdict depends on
+ * the policy).  One pass over d_in (float32, row-major).  d_counts (device
+ * int64[12]) is overwritten: [0] zero padding, [3*kind + gran] for
+ * VLZ_PAD_MIN/MAX/MEAN x VLZ_GRAN_GLOBAL/BLOCK/EDGE.  Stream-ordered. */
+size_t vlz_padding_census_ws_size(const vlz_geom* g);
+int vlz_padding_census(const float* d_in, const vlz_geom* g, double eb, int32_t radius,
+                       int64_t* d_counts, void* d_ws, size_t ws_bytes, void* stream);
+
 /* number of kernel launches the library issued since load (bench evidence) */
 int64_t vlz_launch_count(void);
 /* per-kernel CUDA-event timing: when enabled every launch is bracketed by

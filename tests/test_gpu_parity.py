@@ -276,6 +276,35 @@ def test_outlier_report_matches_reference():
         assert got == c["rows"], c["tag"]
 
 
+@pytest.mark.parametrize("shape,b,radius", [((37, 45, 29), 8, 16), ((300, 170), 16, 32),
+                                             ((5000,), 64, 8), ((20, 70, 130), 32, 64)])
+def test_outlier_report_matches_per_policy_oracle(oracle, shape, b, radius):
+    # the one-pass census (k_census.cu) against ten full oracle compressions,
+    # one per policy, with the border outliers counted from each stream
+    from paper_2201_04614_b200.padding import outlier_report
+    from paper_2201_04614_b200.vector import border_outliers
+
+    rng = np.random.default_rng(sum(shape))
+    idx = np.indices(shape).astype(np.float64)
+    data = sum(np.sin(0.07 * (k + 2) * idx[k]) * 20 for k in range(len(shape)))
+    data = (data + rng.normal(0, 0.4, shape) + 100).astype(np.float32)
+    eb = 1e-2
+    rows = outlier_report(data, _cfg(eb, b, "zero", radius))
+    assert len(rows) == 10
+    zero_total = None
+    for st, red in rows:
+        pol = str(st.policy)
+        o = oracle.dualquant(data, eb, b, radius, pol)
+        grid = M.build_block_grid(M.ArrayDescriptor(len(shape), shape), b)
+        cs = M.CodeStream(o["codes"], o["outlier_values"], o["outlier_counts"], grid, eb, radius,
+                          M.PaddingScalars(st.policy, o["scalars"]))
+        total = int(o["outlier_counts"].sum())
+        assert (st.total_outliers, st.border_outliers) == (total, border_outliers(cs)), pol
+        zero_total = total if zero_total is None else zero_total
+        if zero_total:
+            assert red == 100.0 * (zero_total - total) / zero_total
+
+
 @pytest.mark.parametrize("b", [8, 16, 32, 64, 256])
 def test_fused_1d_kernels(oracle, b):
     # dq_1d.cuh: full tiles through the bulk-copy ring plus a
