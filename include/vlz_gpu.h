@@ -241,6 +241,14 @@ size_t vlz_padding_census_ws_size(const vlz_geom* g);
 int vlz_padding_census(const float* d_in, const vlz_geom* g, double eb, int32_t radius,
                        int64_t* d_counts, void* d_ws, size_t ws_bytes, void* stream);
 
+/* CRC-32 (zlib: polynomial 0xEDB88320 reflected, init/xorout 0xFFFFFFFF) of
+ * n device bytes -- the VLZ1 payload CRC (container.py:160-163, 214-217).
+ * *d_crc (device uint32) receives zlib.crc32(bytes); any alignment; workspace
+ * of vlz_crc32_ws_size(n) device bytes.  Stream-ordered. */
+size_t vlz_crc32_ws_size(int64_t n);
+int vlz_crc32_device(const uint8_t* d_data, int64_t n, uint32_t* d_crc, void* d_ws,
+                     size_t ws_bytes, void* stream);
+
 /* number of kernel launches the library issued since load (bench evidence) */
 int64_t vlz_launch_count(void);
 /* per-kernel CUDA-event timing: when enabled every launch is bracketed by

@@ -85,6 +85,8 @@ PROTOTYPES = {
     "vlz_padding_census_ws_size": (ctypes.c_size_t, [_P(Geom)]),
     "vlz_padding_census": (ctypes.c_int, [_vp, _P(Geom), ctypes.c_double, ctypes.c_int32, _vp,
                                           _vp, ctypes.c_size_t, _vp]),
+    "vlz_crc32_ws_size": (ctypes.c_size_t, [_i64]),
+    "vlz_crc32_device": (ctypes.c_int, [_vp, _i64, _vp, _vp, ctypes.c_size_t, _vp]),
     "vlz_launch_count": (_i64, []),
     "vlz_timing": (None, [ctypes.c_int]),
     "vlz_timing_collect": (ctypes.c_int, [_P(ctypes.c_double), _P(_i64), ctypes.c_int]),

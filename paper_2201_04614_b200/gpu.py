@@ -376,5 +376,28 @@ def border_outliers_device(codes: torch.Tensor, grid, stream=None) -> int:
     return int(total.item())
 
 
+def crc32_device(data: torch.Tensor, nbytes: int | None = None, stream=None) -> int:
+    """zlib.crc32 of the first `nbytes` bytes of a CUDA tensor (any dtype),
+    computed on the device (csrc/k_crc.cu)."""
+    return int(crc32_device_async(data, nbytes, stream).item()) & 0xFFFFFFFF
+
+
+def crc32_device_async(data: torch.Tensor, nbytes: int | None = None, stream=None):
+    """crc32_device without the host synchronisation: returns the int32[1]
+    CUDA tensor the CRC lands in (stream-ordered)."""
+    lib = _lib.load()
+    flat = data.reshape(-1).view(torch.uint8)
+    n = flat.numel() if nbytes is None else int(nbytes)
+    if n > flat.numel():
+        raise ValueError("crc32_device: range past the tensor")
+    ws = torch.empty(int(lib.vlz_crc32_ws_size(n)), dtype=torch.uint8, device=flat.device)
+    out = torch.empty(1, dtype=torch.int32, device=flat.device)
+    rc = lib.vlz_crc32_device(_ptr(flat) if n else None, n, _ptr(out), _ptr(ws), ws.numel(),
+                              _stream(stream))
+    if rc != 0:
+        raise RuntimeError(f"vlz_crc32_device failed ({rc})")
+    return out
+
+
 def launch_count() -> int:
     return int(_lib.load().vlz_launch_count())

@@ -151,9 +151,11 @@ def decode(payload: bytes, bit_length: int, codebook: HuffmanCodebook, count: in
 
 
 def decode_device(payload: bytes, bit_length: int, codebook: HuffmanCodebook, count: int,
-                  device=None):
+                  device=None, device_src=None):
     """decode() on the GPU (csrc/k_huffdec.cu, self-synchronising parallel
-    decode); returns an int16-storage CUDA tensor of `count` uint16 symbols."""
+    decode); returns an int16-storage CUDA tensor of `count` uint16 symbols.
+    `device_src` = (CUDA uint8 tensor, offset): the payload bytes are already
+    on the device there (deserialize(blob, device=...)), no host copy."""
     import torch
 
     from .gpu import _stream
@@ -161,8 +163,12 @@ def decode_device(payload: bytes, bit_length: int, codebook: HuffmanCodebook, co
     lib = _lib.load()
     dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
     nbytes = len(payload)
-    dpay = torch.zeros((nbytes + 3) // 4 * 4 + 16, dtype=torch.uint8, device=dev)
-    if nbytes:
+    dpay = torch.empty((nbytes + 3) // 4 * 4 + 16, dtype=torch.uint8, device=dev)
+    dpay[nbytes:].zero_()  # the decoder reads up to 16 bytes past the payload
+    if nbytes and device_src is not None:
+        src, off = device_src
+        dpay[:nbytes].copy_(src[off: off + nbytes])
+    elif nbytes:
         with warnings.catch_warnings():  # read-only view: only ever read (H2D source)
             warnings.simplefilter("ignore", UserWarning)
             host = torch.frombuffer(payload, dtype=torch.uint8, count=nbytes)

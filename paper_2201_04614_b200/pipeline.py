@@ -126,8 +126,11 @@ def decompress_parsed(parsed: ParsedContainer, thread_count: int = 1):
     grid = build_block_grid(desc, parsed.block_edge)
     cb = parsed.codebook
     if len(cb.lengths) and int(cb.lengths.max()) <= 58:
+        src = None
+        if parsed.device_payload is not None:
+            src = (parsed.device_payload, parsed.device_code_offset)
         codes = decode_device(parsed.code_bits, parsed.code_bit_length, cb, desc.element_count,
-                              device=_device())
+                              device=_device(), device_src=src)
     else:  # empty or pathological book: verdicts from the native host decoder
         codes = decode(parsed.code_bits, parsed.code_bit_length, cb, desc.element_count)
     out = reconstruct_arrays(codes, parsed.outlier_values, parsed.outlier_counts,
@@ -137,5 +140,6 @@ def decompress_parsed(parsed: ParsedContainer, thread_count: int = 1):
 
 
 def decompress(blob: bytes, thread_count: int = 1):
-    """reconstruct.py:127-129: container bytes -> (float32 array, descriptor)."""
-    return decompress_parsed(deserialize(blob), thread_count=thread_count)
+    """reconstruct.py:127-129: container bytes -> (float32 array, descriptor).
+    The payload goes to the GPU once: its CRC and the Huffman decode run there."""
+    return decompress_parsed(deserialize(blob, device=_device()), thread_count=thread_count)

@@ -88,11 +88,12 @@ LARGE = [
 
 @pytest.mark.parametrize("kind,shape,b,pol,eb,radius", LARGE)
 def test_no_out_of_bounds_writes_large_paths(kind, shape, b, pol, eb, radius):
+    prev = M.valid_block_edges()
     M.allow_block_256(True)
     try:
         _run_guarded(_field(kind, shape, b), b, pol, eb, radius)
     finally:
-        M.allow_block_256(False)
+        M.allow_block_256(256 in prev)
 
 
 def _run_guarded(data, b, pol, eb, radius):

@@ -34,7 +34,16 @@ from paper_2201_04614_b200.errors import (  # noqa: E402
 from paper_2201_04614_b200.reconstruct import reconstruct_arrays, reconstruct_stream  # noqa: E402
 from paper_2201_04614_b200.vector import dualquant, dualquant_vector  # noqa: E402
 
-M.allow_block_256(True)
+
+
+@pytest.fixture(autouse=True)
+def _allow_256():
+    # the golden generator allowed block 256 (BASELINE config 1); per test,
+    # so other modules' settings cannot leak in
+    prev = M.valid_block_edges()
+    M.allow_block_256(True)
+    yield
+    M.allow_block_256(256 in prev)
 
 
 def _cfg(eb, b, pol, radius, lanes=8):

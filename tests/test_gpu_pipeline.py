@@ -92,3 +92,39 @@ def test_constant_field_outlier_counts(dims, block):
     grid = M.build_block_grid(M.ArrayDescriptor(len(dims), dims), block)
     assert int(zs.outlier_counts.sum()) == grid.block_count
     assert int(ms.outlier_counts.sum()) == 0
+
+
+def test_device_crc32_equals_zlib():
+    # csrc/k_crc.cu: any length and start alignment, segment boundaries (4 KiB
+    # frames) on both sides, the payload CRC of reference containers
+    import zlib
+
+    from paper_2201_04614_b200.gpu import crc32_device
+
+    rng = np.random.default_rng(4)
+    raw = rng.integers(0, 256, (9 << 20) + 333, dtype=np.uint8)
+    dev = torch.from_numpy(raw).cuda()
+    for off in (0, 1, 3, 7, 8, 15):
+        for n in (0, 1, 2, 15, 16, 17, 4079, 4080, 4095, 4096, 4097, 8192 + 5, 65536 * 3 + 11,
+                  (9 << 20) - off):
+            got = crc32_device(dev[off:off + n], n)
+            assert got == zlib.crc32(raw[off:off + n].tobytes()), (off, n)
+
+
+def test_container_payload_crc_on_device_detects_flips(corpus_cases):
+    # decompress(blob) checks the payload CRC on the device: every flipped
+    # payload byte must be rejected with the reference's PayloadCrcError
+    from paper_2201_04614_b200.container import deserialize
+    from paper_2201_04614_b200.errors import PayloadCrcError
+
+    blobs = [c["blob"].tobytes() for c in corpus_cases if "blob" in c][:8]
+    rng = np.random.default_rng(9)
+    for blob in blobs:
+        p = deserialize(blob, device=torch.device("cuda", 0))
+        assert p.device_payload is not None
+        for _ in range(4):
+            b = bytearray(blob)
+            pos = int(rng.integers(112, len(b) - 4))
+            b[pos] ^= 1 << int(rng.integers(0, 8))
+            with pytest.raises(PayloadCrcError):
+                vlzg.decompress(bytes(b))
