@@ -273,11 +273,62 @@ def cpu_leg(steps: int, warmup: int):
     return 4.0 * sample.size / med / 1e9, med, threads, desc
 
 
+def reference_numpy_leg():
+    """The reference package itself (numpy, installed unmodified into
+    baseline/_ref), on the same CPU sample: its own kernel timer
+    metrics.bench_kernel (metrics.py:193-219; dualquant_vector at lane width
+    16 on every host core, median of 3) for compress, and reconstruct_block
+    (reconstruct.py:30-71) over every 100th block, extrapolated to all blocks,
+    for decompress.  A second stated baseline; None when
+    baseline/_ref is absent."""
+    ref = os.path.join(REPO, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "vlz")):
+        return None
+    sys.path.insert(0, ref)
+    try:
+        import vlz.metrics as vm
+        from vlz.model import CompressionConfig, ErrorBound, PaddingPolicy
+        from vlz.padding import apply_padding
+        from vlz.reconstruct import reconstruct_block
+        from vlz.vector import dualquant_vector
+    except Exception as exc:  # noqa: BLE001 -- report, never fail the arm
+        return {"unavailable": f"import failed: {exc}"}
+    finally:
+        sys.path.remove(ref)
+    from paper_2201_04614_b200 import workloads
+
+    threads = os.cpu_count() or 1
+    sample = workloads.gen_c5_slab_numpy((0, CPU_PLANES))
+    cfg = CompressionConfig(ErrorBound.absolute(C5_EB), block_edge=BLOCK, lane_width=16,
+                            padding=PaddingPolicy.parse(PADDING), radius=RADIUS,
+                            thread_count=threads)
+    t_c = vm.bench_kernel(sample, cfg, repetitions=3).time_s
+    st = dualquant_vector(sample, cfg)
+    grid = st.grid
+    sizes = np.array([int(np.prod(grid.block_extents(b))) for b in range(grid.block_count)])
+    cs = np.concatenate([[0], np.cumsum(sizes)])
+    os_ = np.concatenate([[0], np.cumsum(st.outlier_counts)])
+    picks = range(0, grid.block_count, 100)
+    t0 = time.perf_counter()
+    for b in picks:
+        reconstruct_block(st.codes[cs[b]:cs[b + 1]], st.outlier_values[os_[b]:os_[b + 1]],
+                          apply_padding(st.scalars, grid, b), grid.block_extents(b), C5_EB, RADIUS)
+    t_d = (time.perf_counter() - t0) * grid.block_count / len(picks)
+    nb = 4.0 * sample.size
+    return {"kind": "reference", "impl": "vlz (numpy) from baseline/_ref, unmodified",
+            "compress_gbs": nb / t_c / 1e9, "decompress_gbs_extrapolated": nb / t_d / 1e9,
+            "round_trip_gbs": nb / (t_c + t_d) / 1e9, "cores": threads,
+            "sample": f"C5 slab {sample.shape[0]}x{SHAPE[1]}x{SHAPE[2]}; compress by "
+                      f"metrics.bench_kernel (median of 3), decompress by reconstruct_block on "
+                      f"{len(picks)} of {grid.block_count} blocks, extrapolated"}
+
+
 def run_reference(args):
     ws, rank, local = dist_env()
     if rank != 0:
         return  # the reference arm runs on rank 0 only
     value, med, threads, desc = cpu_leg(args.steps, args.warmup)
+    numpy_ref = None if args.no_cpu_baseline else reference_numpy_leg()
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -287,6 +338,7 @@ def run_reference(args):
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "port",
                          "sample": desc},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_numpy": numpy_ref,
     }
     print(json.dumps(line), flush=True)
 
