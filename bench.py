@@ -353,7 +353,7 @@ def workload_config(n, eb):
 
 def run_cpu_check(args):
     """The GPU arm's multi-rank orchestration on CPU: gloo ranks, value
-    range all-reduce, mean:global statistics all-gather (sharded.reduce_stats),
+    range all-reduce, mean:global statistics all-gather (sharded.gather_stats),
     the pinned CPU oracle as each shard's compressor, piece hashes gathered on
     rank 0 into the stream digest.  tests/test_bench_cpu.py runs it at 1 and 2
     ranks and requires the same digest (and the single-process oracle's)."""
@@ -364,7 +364,7 @@ def run_cpu_check(args):
     import oracle
 
     from paper_2201_04614_b200 import workloads
-    from paper_2201_04614_b200.sharded import reduce_stats
+    from paper_2201_04614_b200.sharded import gather_stats, reduce_gathered
 
     ws, rank, _ = dist_env()
     if ws > 1:
@@ -383,7 +383,7 @@ def run_cpu_check(args):
     st = oracle.global_stats(x, eb)
     stats = torch.tensor([st[0], st[1], st[2], -st[3]], dtype=torch.int64)
     if ws > 1:
-        reduce_stats(stats)
+        stats = reduce_gathered(gather_stats(stats))  # as the finish kernel reduces
     s0 = oracle.stat_value("mean", int(stats[0]), int(stats[1]), int(stats[2]), -int(stats[3]))
     o = oracle.dualquant(x, eb, BLOCK, RADIUS, PADDING, threads=1, global_scalar=s0)
     per_layer = -(-shape[1] // BLOCK) * -(-shape[2] // BLOCK)
@@ -457,6 +457,7 @@ def run_ours(args):
     wsb = lib.vlz_workspace_size(ctypes.byref(g))
     wspace = torch.empty(wsb, dtype=torch.uint8, device=dev)
     totals = torch.empty(ws, dtype=torch.int64, device=dev)
+    gathered = torch.empty(4 * ws, dtype=torch.int64, device=dev)
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream
     evs = []  # per timed step: (start, compress done, decompress done)
@@ -473,14 +474,15 @@ def run_ours(args):
                                        codes.data_ptr(), counts.data_ptr(), scalars.data_ptr(),
                                        res.data_ptr(), stats.data_ptr(), wspace.data_ptr(), wsb, sp)
         assert rc == 0
-        if ws > 1:  # padding statistics of all shards: one all-gather, reduced locally
-            from paper_2201_04614_b200.sharded import reduce_stats
-
-            reduce_stats(stats)
-        rc = lib.vlz_dq_compress_finish(x.data_ptr(), ctypes.byref(g), ctypes.byref(p),
-                                        stats.data_ptr(), codes.data_ptr(), outl.data_ptr(),
-                                        counts.data_ptr(), scalars.data_ptr(), res.data_ptr(),
-                                        wspace.data_ptr(), wsb, sp)
+        fs = stats
+        if ws > 1:  # padding statistics of all shards: one all-gather, reduced in the finish kernel
+            dist.all_gather_into_tensor(gathered, stats)
+            fs = gathered
+        rc = lib.vlz_dq_compress_finish_gathered(x.data_ptr(), ctypes.byref(g), ctypes.byref(p),
+                                                 fs.data_ptr(), fs.numel() // 4, codes.data_ptr(),
+                                                 outl.data_ptr(), counts.data_ptr(),
+                                                 scalars.data_ptr(), res.data_ptr(),
+                                                 wspace.data_ptr(), wsb, sp)
         assert rc == 0
         if ws > 1:  # per-shard outlier totals -> global offsets (metadata)
             dist.all_gather_into_tensor(totals, res[2:3])

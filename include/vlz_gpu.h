@@ -127,6 +127,15 @@ int vlz_dq_compress_finish(const float* d_in, const vlz_geom* g, const vlz_param
                            const vlz_stats* d_global_stats, uint16_t* d_codes,
                            float* d_outliers, int64_t* d_counts, int64_t* d_scalars,
                            vlz_result* d_result, void* d_ws, size_t ws_bytes, void* stream);
+/* As finish, with the statistics of every rank as gathered (one all-gather
+ * of nranks vlz_stats records, rank order) instead of pre-reduced: the
+ * reduction (wrapping sum, count, min, min of -max) runs inside the scan
+ * kernel, so a sharded step needs no reduction kernels of its own. */
+int vlz_dq_compress_finish_gathered(const float* d_in, const vlz_geom* g, const vlz_params* p,
+                                    const vlz_stats* d_rank_stats, int32_t nranks,
+                                    uint16_t* d_codes, float* d_outliers, int64_t* d_counts,
+                                    int64_t* d_scalars, vlz_result* d_result, void* d_ws,
+                                    size_t ws_bytes, void* stream);
 
 /* ---- decompress: replaces reconstruct.decompress_parsed minus the Huffman
  * decode (reconstruct.py:30-124).  Codes uint16 (container symbol width) or

@@ -53,6 +53,9 @@ PROTOTYPES = {
                                              _vp, ctypes.c_size_t, _vp]),
     "vlz_dq_compress_finish": (ctypes.c_int, [_vp, _P(Geom), _P(Params), _vp, _vp, _vp, _vp, _vp,
                                               _vp, _vp, ctypes.c_size_t, _vp]),
+    "vlz_dq_compress_finish_gathered": (ctypes.c_int, [_vp, _P(Geom), _P(Params), _vp,
+                                                       ctypes.c_int32, _vp, _vp, _vp, _vp, _vp,
+                                                       _vp, ctypes.c_size_t, _vp]),
     "vlz_dq_decompress": (ctypes.c_int, [_vp, _vp, _i64, _vp, _vp, _P(Geom), _P(Params), _vp, _vp,
                                          _vp, ctypes.c_size_t, _vp]),
     "vlz_dq_decompress_u32": (ctypes.c_int, [_vp, _vp, _i64, _vp, _vp, _P(Geom), _P(Params), _vp,

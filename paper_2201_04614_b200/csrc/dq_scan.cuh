@@ -57,7 +57,8 @@ struct ScanArgs {
   unsigned long long* lb;  // per chunk look-back words
   unsigned int* ticket;
   long long* n_out;
-  const long long* gstats;  // sum, count, min, neg_max (reduced)
+  const long long* gstats;  // sum, count, min, neg_max per record (nstats records:
+  int nstats;               // one reduced record, or one per rank when sharded)
   // compress status finalisation (done by the chunk holding the last block)
   int* status;
   long long* index;
@@ -212,8 +213,19 @@ __global__ void __launch_bounds__(SCAN_THREADS) dq_scan_kernel(ScanArgs a) {
 
   int64_t s0 = 0;
   if (fix) {
+    // the records of all ranks (or the single reduced one) reduced here, as
+    // np.sum / min / max over the whole field (padding.py:62-69): the sum
+    // wraps in int64 like the reference's
     const long long* gs = a.gstats;
-    s0 = stat_value(a.q.kind, gs[0], gs[1], gs[2], -gs[3]);
+    unsigned long long sum = (unsigned long long)gs[0];
+    long long cnt = gs[1], mn = gs[2], nmx = gs[3];
+    for (int r = 1; r < a.nstats; ++r) {
+      sum += (unsigned long long)gs[4 * r];
+      cnt += gs[4 * r + 1];
+      mn = gs[4 * r + 2] < mn ? gs[4 * r + 2] : mn;
+      nmx = gs[4 * r + 3] < nmx ? gs[4 * r + 3] : nmx;
+    }
+    s0 = stat_value(a.q.kind, (long long)sum, cnt, mn, -nmx);
   }
 
 #pragma unroll

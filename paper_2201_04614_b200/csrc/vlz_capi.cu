@@ -414,11 +414,26 @@ __attribute__((visibility("hidden"))) int vlz_internal_compress_begin(const floa
   return to_rc(e);
 }
 
+static int finish_impl(const float* d_in, const vlz_geom* gg, const vlz_params* p,
+                       const long long* gstats, int nstats, uint16_t* d_codes,
+                       float* d_outliers, int64_t* d_counts, int64_t* d_scalars,
+                       vlz_result* d_result, void* d_ws, size_t ws_bytes, cudaStream_t st,
+                       unsigned long long* patch_list, unsigned int* patch_count);
+
 __attribute__((visibility("hidden"))) int vlz_internal_compress_finish(const float* d_in, const vlz_geom* gg, const vlz_params* p,
                                 const long long* gstats, uint16_t* d_codes, float* d_outliers,
                                 int64_t* d_counts, int64_t* d_scalars, vlz_result* d_result,
                                 void* d_ws, size_t ws_bytes, cudaStream_t st,
                                 unsigned long long* patch_list, unsigned int* patch_count) {
+  return finish_impl(d_in, gg, p, gstats, 1, d_codes, d_outliers, d_counts, d_scalars, d_result,
+                     d_ws, ws_bytes, st, patch_list, patch_count);
+}
+
+static int finish_impl(const float* d_in, const vlz_geom* gg, const vlz_params* p,
+                       const long long* gstats, int nstats, uint16_t* d_codes,
+                       float* d_outliers, int64_t* d_counts, int64_t* d_scalars,
+                       vlz_result* d_result, void* d_ws, size_t ws_bytes, cudaStream_t st,
+                       unsigned long long* patch_list, unsigned int* patch_count) {
   Geo g;
   if (!make_geo(gg, g, true) || !valid_params(p) || !d_outliers || !d_result || !d_ws)
     return VLZ_E_ARG;
@@ -445,6 +460,8 @@ __attribute__((visibility("hidden"))) int vlz_internal_compress_finish(const flo
   s.ticket = w.ticket;
   s.n_out = reinterpret_cast<long long*>(&d_result->n_outliers);
   s.gstats = gstats;
+  s.nstats = nstats;
+  if (nstats < 1) return VLZ_E_ARG;
   s.status = &d_result->status;
   s.index = reinterpret_cast<long long*>(&d_result->index);
   s.first_nonfinite = reinterpret_cast<const unsigned long long*>(&d_result->first_nonfinite);
@@ -476,6 +493,16 @@ int vlz_dq_compress_begin(const float* d_in, const vlz_geom* g, const vlz_params
   return vlz_internal_compress_begin(d_in, g, p, d_codes, d_counts, d_scalars, d_result,
                              reinterpret_cast<long long*>(d_stats), d_ws, ws_bytes,
                              static_cast<cudaStream_t>(stream));
+}
+
+int vlz_dq_compress_finish_gathered(const float* d_in, const vlz_geom* g, const vlz_params* p,
+                                    const vlz_stats* d_rank_stats, int32_t nranks,
+                                    uint16_t* d_codes, float* d_outliers, int64_t* d_counts,
+                                    int64_t* d_scalars, vlz_result* d_result, void* d_ws,
+                                    size_t ws_bytes, void* stream) {
+  return finish_impl(d_in, g, p, reinterpret_cast<const long long*>(d_rank_stats), nranks,
+                     d_codes, d_outliers, d_counts, d_scalars, d_result, d_ws, ws_bytes,
+                     static_cast<cudaStream_t>(stream), nullptr, nullptr);
 }
 
 int vlz_dq_compress_finish(const float* d_in, const vlz_geom* g, const vlz_params* p,

@@ -10,9 +10,9 @@ order, byte-identical to the single-GPU stream.
 Collectives (torch.distributed; NCCL on GPUs, gloo in the CPU tests):
   * relative error bound: all-reduce MIN/MAX of the shard value ranges
     (model.py:104-110) -- before compression, like the reference;
-  * *:global padding: all-reduce of the partial statistics
-    (SUM of the wrapping int64 sum and of the count, MIN of min and of -max,
-    padding.py:62-85) between the fused kernel and the origin fix-up;
+  * *:global padding: one all-gather of the partial statistics (sum,
+    count, min, -max per rank, padding.py:62-85) between the fused kernel and
+    the origin fix-up; the finish kernel reduces the gathered records;
   * all-gather of the per-shard outlier totals -> each shard's offset into
     the global outlier array (CodeStream.outlier_values).
 Bulk data never crosses GPUs.
@@ -74,18 +74,29 @@ def _reduce_range(lo: float, hi: float, group, device):
     return float(t[0]), -float(t[1])
 
 
-def reduce_stats(stats: torch.Tensor, group=None):
-    """In place: [sum, count] summed, [min, -max] minimised across ranks.
-
-    One collective per step: an all-gather of every rank's 4 words (32 B),
-    reduced locally, instead of a SUM and a MIN all-reduce (each collective
-    costs a launch-latency-bound round trip at 8 GPUs)."""
+def gather_stats(stats: torch.Tensor, group=None) -> torch.Tensor:
+    """Every rank's 4 statistic words [sum, count, min, -max] in rank order
+    (int64 [world * 4]): the one collective of a *:global step (32 B per rank,
+    one all-gather instead of a SUM and a MIN all-reduce).  The reduction runs
+    inside the finish kernel (vlz_dq_compress_finish_gathered)."""
     world = dist.get_world_size(group)
     allst = torch.empty(world * 4, dtype=stats.dtype, device=stats.device)
     dist.all_gather_into_tensor(allst, stats.contiguous(), group=group)
-    allst = allst.view(world, 4)
-    stats[0:2] = allst[:, 0:2].sum(dim=0)  # int64 wraps like the reference's np.sum
-    stats[2:4] = allst[:, 2:4].min(dim=0).values
+    return allst
+
+
+def reduce_gathered(allst: torch.Tensor) -> torch.Tensor:
+    """Host-side form of the finish kernel's reduction of gathered records:
+    [sum, count] summed (int64 wraps like the reference's np.sum), [min,
+    -max] minimised.  For backends without the fused reduction (tests)."""
+    a = allst.view(-1, 4)
+    return torch.cat([a[:, 0:2].sum(dim=0), a[:, 2:4].min(dim=0).values])
+
+
+def reduce_stats(stats: torch.Tensor, group=None):
+    """In place: the statistics of all ranks reduced (gather_stats +
+    reduce_gathered)."""
+    stats.copy_(reduce_gathered(gather_stats(stats, group)))
     return stats
 
 
@@ -128,12 +139,15 @@ class GpuBackend:
         return h
 
     def finish(self, h, stats):
+        """`stats`: one reduced record or the gathered records of all ranks
+        (int64 [nranks * 4]); the scan kernel reduces them."""
         st = torch.cuda.current_stream().cuda_stream
-        rc = self.lib.vlz_dq_compress_finish(
+        stats = stats.contiguous()
+        rc = self.lib.vlz_dq_compress_finish_gathered(
             h["x"].data_ptr(), ctypes.byref(h["g"]), ctypes.byref(h["p"]), stats.data_ptr(),
-            h["codes"].data_ptr(), h["outliers"].data_ptr(), h["counts"].data_ptr(),
-            h["scalars"].data_ptr(), h["result"].data_ptr(), h["ws"].data_ptr(), h["ws"].numel(),
-            st)
+            stats.numel() // 4, h["codes"].data_ptr(), h["outliers"].data_ptr(),
+            h["counts"].data_ptr(), h["scalars"].data_ptr(), h["result"].data_ptr(),
+            h["ws"].data_ptr(), h["ws"].numel(), st)
         if rc != 0:
             raise RuntimeError(f"vlz_dq_compress_finish failed ({rc})")
         return h
@@ -174,7 +188,7 @@ def compress_sharded(x_local: torch.Tensor, full_shape, config: CompressionConfi
     pol = config.padding
     stats = h["stats"]
     if pol.value_kind is not PaddingValue.ZERO and pol.granularity is PaddingGranularity.GLOBAL:
-        reduce_stats(stats, group)
+        stats = gather_stats(stats, group)  # reduced by the finish kernel
     backend.finish(h, stats)
     totals = torch.empty(world, dtype=torch.int64, device=dev)
     dist.all_gather_into_tensor(totals, backend.n_outliers(h), group=group)

@@ -50,8 +50,10 @@ def test_shards_concatenate_to_single_stream(pol, world):
         hs.append(be.begin(x, g, eb, cfg))
     stats = torch.stack([h["stats"] for h in hs])
     red = torch.stack([stats[:, 0].sum(), stats[:, 1].sum(), stats[:, 2].min(), stats[:, 3].min()])
-    for h in hs:
-        be.finish(h, red.clone())
+    for i, h in enumerate(hs):
+        # odd shards: the gathered records of all ranks, reduced in the finish
+        # kernel (vlz_dq_compress_finish_gathered); even: pre-reduced record
+        be.finish(h, stats.reshape(-1).clone() if i % 2 else red.clone())
     torch.cuda.synchronize()
     codes, outl, counts, scal = [], [], [], []
     for h in hs:

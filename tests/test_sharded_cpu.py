@@ -53,11 +53,13 @@ class OracleBackend:
         return {"x": x, "grid": grid, "eb": eb, "config": config, "stats": stats}
 
     def finish(self, h, stats):
+        from paper_2201_04614_b200.sharded import reduce_gathered
+
         cfg = h["config"]
         pol = str(cfg.padding)
         s0 = None
         if pol.endswith(":global") and not pol.startswith("zero"):
-            s = stats.tolist()
+            s = reduce_gathered(stats).tolist()  # the GPU finish kernel's reduction
             s0 = self.o.stat_value(pol.split(":")[0], s[0], s[1], s[2], -s[3])
         h["stream"] = self.o.dualquant(h["x"].numpy(), h["eb"], cfg.block_edge, cfg.radius, pol,
                                        threads=1, global_scalar=s0)
