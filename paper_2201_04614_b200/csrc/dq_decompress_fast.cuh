@@ -29,6 +29,10 @@
 //    one tensor load per plane brings 16 block planes, 128-byte swizzled.
 #pragma once
 
+#ifndef VLZ_SENT_PAIRED
+#define VLZ_SENT_PAIRED 1  // sentinel quotients in paired FP32 (0: scalar quant_fast; A/B on B200: C5 equal, stress 78.1 vs 78.2 us)
+#endif
+
 #include "dq_compress_fast.cuh"
 #include "dq_decompress.cuh"
 
@@ -349,36 +353,64 @@ __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, c
         for (int j = 0; j < VPL; ++j) smask |= (c[j] == 0u) ? (1u << j) : 0u;
         int tot;
         const int excl = group_excl_scan<LPB>(__popc(smask), lane, tot);
-        int k = run + excl;
+        // all of the row's outlier loads first (independent, predicated
+        // addresses: the j-th sentinel of the lane is outlier run + excl +
+        // popc(smask below j)), so they are in flight together
+#pragma unroll
+        for (int j = 0; j < VPL; ++j) {
+          const long long kj = run + excl + __popc(smask & ((1u << j) - 1u));
+          vs[j] = (((smask >> j) & 1u) && kj < avail) ? __ldg(a.outliers + off + kj) : 0.f;
+        }
+        // d of every sentinel value, branch free: the compress side's
+        // exact-fast quotient in paired FP32 (equal to round_half_away(fl64(v
+        // / 2eb)) whenever it reports ok) ...
+        int dsv[VPL];
+        unsigned okm = 0;
+#if VLZ_SENT_PAIRED
+#pragma unroll
+        for (int j = 0; j < VPL; j += 2) {
+          const float2 qq = __fmul2_rn(make_float2(vs[j], vs[j + 1]),
+                                       make_float2(a.q.inv32, a.q.inv32));
+          const float2 r = __fadd2_rn(qq, make_float2(12582912.0f, 12582912.0f));
+          const float2 rn = __fadd2_rn(r, make_float2(-12582912.0f, -12582912.0f));
+          const float2 e = __ffma2_rn(rn, make_float2(-1.0f, -1.0f), qq);
+          const float2 lim = __ffma2_rn(make_float2(fabsf(qq.x), fabsf(qq.y)),
+                                        make_float2(-a.q.kq, -a.q.kq),
+                                        make_float2(a.q.lim0, a.q.lim0));
+          dsv[j] = __float_as_int(r.x) - 0x4B400000;
+          dsv[j + 1] = __float_as_int(r.y) - 0x4B400000;
+          okm |= (fabsf(e.x) < lim.x ? 1u : 0u) << j;
+          okm |= (fabsf(e.y) < lim.y ? 2u : 0u) << j;
+        }
+#else
+#pragma unroll
+        for (int j = 0; j < VPL; ++j) {
+          bool qok;
+          dsv[j] = quant_fast(vs[j], a.q, qok);
+          okm |= qok ? (1u << j) : 0u;
+        }
+#endif
+        // ... and the fp64 division for the sentinels it rejects (rare)
+        const unsigned need = smask & ~okm;
+        if (__any_sync(FULL, need != 0u)) {
+#pragma unroll
+          for (int j = 0; j < VPL; ++j) {
+            if ((need >> j) & 1u) {
+              const long long ds = quant_value(vs[j], a.q.twoeb);
+              wide |= (ds >= (1ll << 27)) || (ds <= -(1ll << 27));
+              dsv[j] = (int)ds;
+            }
+          }
+        }
         int acc = 0;
         unsigned before = 0;
         bool reset = false;
-        // all of the row's outlier loads first (independent addresses), so
-        // they are in flight together, then the quantisation and the resets
 #pragma unroll
         for (int j = 0; j < VPL; ++j) {
-          vs[j] = 0.f;
-          if ((smask >> j) & 1u) {
-            if (k < avail) vs[j] = __ldg(a.outliers + off + k);
-            ++k;
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < VPL; ++j) {
-          if ((smask >> j) & 1u) {
-            // the compress side's exact-fast quotient (quant_fast: equal to
-            // round_half_away(fl64(v / 2eb)) whenever it reports ok); the fp64
-            // division only for the rest
-            bool qok;
-            const int nq = quant_fast(vs[j], a.q, qok);
-            const long long ds = qok ? (long long)nq : quant_value(vs[j], a.q.twoeb);
-            wide |= (ds >= (1ll << 27)) || (ds <= -(1ll << 27));
-            acc = (int)ds - ep[j] - grow[j];
-            reset = true;
-          } else {
-            acc += (int)c[j] - R;
-          }
-          if (!reset) before |= 1u << j;
+          const bool sj = (smask >> j) & 1u;
+          acc = sj ? dsv[j] - ep[j] - grow[j] : acc + ((int)c[j] - R);
+          reset = reset || sj;
+          before |= reset ? 0u : (1u << j);
           h[j] = acc;
         }
         run += tot;
