@@ -2,6 +2,8 @@
 #include "dq_1d.cuh"
 #include "launch.cuh"
 
+#include <cstdlib>
+
 namespace vlz {
 
 template <typename Kern>
@@ -68,10 +70,16 @@ static cudaError_t run_c1d_b(int mode, const CompressArgs& a, cudaStream_t st) {
 
 // below ~4 M elements the call is launch bound: one generic kernel beats the
 // fused kernel + its (usually empty) int64 redo launch
-constexpr int64_t D1_MIN_N = 1ll << 22;
+static int64_t d1_min_n() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("VLZ_D1_MIN_N");  // A/B runs of the threshold
+    return e ? (int64_t)std::atoll(e) : (1ll << 22);
+  }();
+  return v;
+}
 
 bool d1_fast_compress_ok(const CompressArgs& a) {
-  return a.g.D2 >= D1_MIN_N && a.redo_list != nullptr && (reinterpret_cast<uintptr_t>(a.in) & 15) == 0 &&
+  return a.g.D2 >= d1_min_n() && a.redo_list != nullptr && (reinterpret_cast<uintptr_t>(a.in) & 15) == 0 &&
          (reinterpret_cast<uintptr_t>(a.codes) & 15) == 0 && a.g.D2 < (1ll << 40) &&
          (a.g.D2 + D1_TILE - 1) / D1_TILE < (1ll << 31);
 }
@@ -124,7 +132,7 @@ static cudaError_t run_d1d(const DecompressArgs& a, cudaStream_t st) {
 }
 
 bool d1_fast_decompress_ok(bool u32, const DecompressArgs& a) {
-  return a.g.D2 >= D1_MIN_N && !u32 && a.redo_list != nullptr && (reinterpret_cast<uintptr_t>(a.codes) & 15) == 0 &&
+  return a.g.D2 >= d1_min_n() && !u32 && a.redo_list != nullptr && (reinterpret_cast<uintptr_t>(a.codes) & 15) == 0 &&
          (reinterpret_cast<uintptr_t>(a.out) & 15) == 0 && a.g.D2 < (1ll << 40) &&
          (a.g.D2 + D1_TILE - 1) / D1_TILE < (1ll << 31) && a.q.twoeb < 1e300;
 }

@@ -152,6 +152,19 @@ def main():
             f += np.sin(2 * np.pi * (ky * y + kx * x) + rng.uniform(0, 6.28)).astype(np.float32)
         run("2D 16384^2 b=16 mean:block", f, 1e-4, 16, "mean:block", 512)
         run("2D 16384^2 b=8 zero", f, 1e-4, 8, "zero", 512)
+    if "big" in which:  # block edges 32 / 64 (tools/bench_bigblocks.py cases)
+        c4 = workloads.gen_c4(512)
+        for b in (32, 64):
+            run(f"C4 512^3 b={b}", c4, 1e-3, b, "mean:global", 512)
+        rng = np.random.default_rng(6)
+        y, x = np.meshgrid(np.linspace(0, 1, 8192, dtype=np.float32),
+                           np.linspace(0, 1, 8192, dtype=np.float32), indexing="ij")
+        f = np.zeros((8192, 8192), np.float32)
+        for _ in range(8):
+            ky, kx = rng.integers(1, 16, 2)
+            f += np.sin(2 * np.pi * (ky * y + kx * x) + rng.uniform(0, 6.28)).astype(np.float32)
+        for b in (32, 64):
+            run(f"2D 8192^2 b={b}", f, 1e-4, b, "mean:block", 512)
     if "stress" in which:
         c4 = workloads.gen_c4(256)
         run("stress b=8 R=512 eb=1e-5", c4, 1e-5, 8, "mean:global", 512)
