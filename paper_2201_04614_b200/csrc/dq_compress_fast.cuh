@@ -29,6 +29,12 @@
 namespace vlz {
 
 constexpr int FAST_STAGES = 2;
+#ifndef VLZ_BIG_BATCH_C
+#define VLZ_BIG_BATCH_C 1  // 3-D b >= 32 compress: interior stage rows in batches
+#endif                     // (512^3 b=64 564 -> 318 us, b=32 193 -> 148 us; 2-D slower: off)
+#ifndef VLZ_BATCH_ROWS
+#define VLZ_BATCH_ROWS 8  // rows per batch (divides the 8-row stage; 4: b=64 337 us)
+#endif
 constexpr int FAST_WARPS = 4;
 
 // per-lane vector moves of VPL (2, 4, 8) consecutive 32-bit values
@@ -282,8 +288,149 @@ __device__ __forceinline__ void fast_tile(const FastArgs& fa, uint32_t tile, con
       d_origin = n0;
       bad_origin = ob;
     }
+    int rstart = 0;  // first row of the stage for the per-row loop
+    constexpr bool BATCH = VLZ_BIG_BATCH_C && INTERIOR && F::SPLIT > 1 && ND == 3;
+#if VLZ_BIG_BATCH_C
+    if constexpr (BATCH) {
+#pragma unroll 1
+      for (int h = 0; h < F::STAGE_ROWS; h += VLZ_BATCH_ROWS) {
+      // b >= 32 interior stage as one batch: few tiles (512^3 b=64 is one
+      // warp per block, ~3.5 warps per SM) leave each row's dependent chain
+      // exposed; the rows' loads, quotients, x-shuffles and plane accesses
+      // are independent and interleave here, only Dy runs in row order.  A
+      // stage with an element off the fast quotient takes the per-row loop.
+      constexpr int RB = VLZ_BATCH_ROWS;
+      float vb[RB][VPL];
+      unsigned nbb[RB][VPL];
+      bool okb = true;
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        ld_vec<VPL>(plane + (h + r) * W, vb[r]);
+#pragma unroll
+        for (int j = 0; j < VPL; j += 2) {
+          const float2 qq = __fmul2_rn(make_float2(vb[r][j], vb[r][j + 1]),
+                                       make_float2(q.inv32, q.inv32));
+          const float2 rr = __fadd2_rn(qq, make_float2(12582912.0f, 12582912.0f));
+          nbb[r][j] = __float_as_uint(rr.x);
+          nbb[r][j + 1] = __float_as_uint(rr.y);
+          const float2 rn = __fadd2_rn(rr, make_float2(-12582912.0f, -12582912.0f));
+          const float2 e = __ffma2_rn(rn, make_float2(-1.0f, -1.0f), qq);
+          const float2 lim = __ffma2_rn(make_float2(fabsf(qq.x), fabsf(qq.y)),
+                                        make_float2(-q.kq, -q.kq), make_float2(q.lim0, q.lim0));
+          okb = okb && (fabsf(e.x) < lim.x) && (fabsf(e.y) < lim.y);
+        }
+      }
+      if (__all_sync(FULL, okb)) {
+        int dlb[RB][VPL];
+#pragma unroll
+        for (int r = 0; r < RB; ++r) {
+          unsigned left = __shfl_up_sync(FULL, nbb[r][VPL - 1], 1);
+          if (xhead) left = MAGIC_BITS;
+          dlb[r][0] = (int)(nbb[r][0] - left);
+#pragma unroll
+          for (int j = 1; j < VPL; ++j) dlb[r][j] = (int)(nbb[r][j] - nbb[r][j - 1]);
+        }
+#pragma unroll
+        for (int r = 0; r < RB; ++r) {
+#pragma unroll
+          for (int j = 0; j < VPL; ++j) {
+            const int t = dlb[r][j] - prow[j];
+            prow[j] = dlb[r][j];
+            dlb[r][j] = t;
+          }
+        }
+        if (ND == 3) {
+#pragma unroll
+          for (int r = 0; r < RB; ++r) {
+            int* pp = pplane + (part * F::STAGE_ROWS + h + r) * W;
+            int prev[VPL];
+            ld_vec<VPL>(pp, prev);
+            st_vec<VPL>(pp, dlb[r]);
+#pragma unroll
+            for (int j = 0; j < VPL; ++j) dlb[r][j] -= prev[j];
+          }
+        }
+        unsigned ub[RB][VPL];
+        unsigned umax = 0;
+#pragma unroll
+        for (int r = 0; r < RB; ++r)
+#pragma unroll
+          for (int j = 0; j < VPL; ++j) {
+            ub[r][j] = (unsigned)(dlb[r][j] + (R - 1));
+            umax = ub[r][j] > umax ? ub[r][j] : umax;
+          }
+        unsigned cadd_rows = 0xffu;  // bit r: row r takes the common +1 in its packed store
+        if (__any_sync(FULL, umax > span)) {
+          // rare: outliers, ranked inside the block in traversal order
+#pragma unroll
+          for (int r = 0; r < RB; ++r) {
+            const int yl = part * F::STAGE_ROWS + h + r;
+            unsigned rmax = 0;
+#pragma unroll
+            for (int j = 0; j < VPL; ++j) rmax = ub[r][j] > rmax ? ub[r][j] : rmax;
+            if (!__any_sync(FULL, rmax > span)) continue;
+            unsigned om = 0;
+#pragma unroll
+            for (int j = 0; j < VPL; ++j) {
+              const bool o = ub[r][j] > span;
+              ub[r][j] = o ? 0u : ub[r][j] + 1u;
+              om |= o ? (1u << j) : 0u;
+            }
+            cadd_rows &= ~(1u << r);
+            if ((zl == 0) && (yl == 0) && xhead) om &= ~1u;  // the origin is settled at the tile end
+            int tot;
+            const int excl = group_excl_scan<LPB>(__popc(om), lane, tot);
+            int k = run + excl;
+            float* slot = a.scratch + bstart + 1;
+#pragma unroll
+            for (int j = 0; j < VPL; ++j)
+              if ((om >> j) & 1u) slot[k++] = vb[r][j];
+            run += tot;
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < RB; ++r) {
+          st_codes<VPL>(cptr, ub[r], ((cadd_rows >> r) & 1u) ? 0x00010001u : 0u);
+          cptr += ex;
+          const int yl = part * F::STAGE_ROWS + h + r;
+          if (MODE == MODE_GLOBAL) {
+            if (K == 3) {
+              unsigned rs = nbb[r][0];
+#pragma unroll
+              for (int j = 1; j < VPL; ++j) rs += nbb[r][j];
+              psum += (int)(rs - (unsigned)VPL * MAGIC_BITS);
+            } else {
+#pragma unroll
+              for (int j = 0; j < VPL; ++j) tacc.add((int)(nbb[r][j] - MAGIC_BITS));
+            }
+          } else if (MODE == MODE_BLOCK) {
+#pragma unroll
+            for (int j = 0; j < VPL; ++j) face[0].add((int)(nbb[r][j] - MAGIC_BITS));
+          } else if (MODE == MODE_EDGE) {
+#pragma unroll
+            for (int j = 0; j < VPL; ++j) {
+              const int d = (int)(nbb[r][j] - MAGIC_BITS);
+              const bool x0 = (xin + j) == 0;
+              if (ND == 3) {
+                if (zl == 0) face[0].add(d);
+                if (yl == 0) face[1 % ND].add(d);
+                if (x0) face[ND - 1].add(d);
+              } else {
+                if (yl == 0) face[0].add(d);
+                if (x0) face[ND - 1].add(d);
+              }
+            }
+          }
+        }
+        rstart = h + RB;
+      } else {
+        break;  // rows h.. take the per-row loop
+      }
+      }
+    }
+#endif
 #pragma unroll 2
-    for (int r = 0; r < F::STAGE_ROWS; ++r) {
+    for (int r = BATCH ? rstart : 0; r < F::STAGE_ROWS; ++r) {
       const int yl = part * F::STAGE_ROWS + r;
       if (!INTERIOR && yl >= ey) break;
       float v[VPL];

@@ -29,6 +29,10 @@
 //    one tensor load per plane brings 16 block planes, 128-byte swizzled.
 #pragma once
 
+#ifndef VLZ_BIG_BATCH
+#define VLZ_BIG_BATCH 1  // b >= 32 decompress: sentinel-free 8-row stages as one batch
+                         // (512^3 b=64 799 -> 318 us, b=32 260 -> 180 us; 2-D unchanged)
+#endif
 #ifndef VLZ_SENT_PAIRED
 #define VLZ_SENT_PAIRED 1  // sentinel quotients in paired FP32 (0: scalar quant_fast; A/B on B200: C5 equal, stress 78.1 vs 78.2 us)
 #endif
@@ -295,6 +299,94 @@ __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, c
           slot = slot0 + cons.stage * F::STAGE_BYTES;
           cp_async_wait<DSTAGES - 1>();
         }
+#if VLZ_BIG_BATCH
+        // b >= 32: few tiles (512^3 b=64 is one warp per block, ~3.5 warps
+        // per SM), so a row's dependent chain -- the x-scan's shuffles, the
+        // plane load, the dequantisation -- is exposed.  A stage without
+        // sentinels runs its STAGE_ROWS rows as one batch: the x-scans are
+        // independent and interleave; only the y/z accumulation is sequential.
+        if (yl % F::STAGE_ROWS == 0 && yl + F::STAGE_ROWS <= ey) {
+          constexpr int RB = F::STAGE_ROWS;
+          unsigned cb[RB][VPL];
+          unsigned cmn = 0xffffffffu;
+#pragma unroll
+          for (int r = 0; r < RB; ++r) {
+            const unsigned char* rp = slot + r * 32 * F::LANE_BYTES;
+            if (VPL == 4) {
+              const uint2 pk = *reinterpret_cast<const uint2*>(rp);
+              cb[r][0] = pk.x & 0xffffu; cb[r][1 % VPL] = pk.x >> 16;
+              cb[r][2 % VPL] = pk.y & 0xffffu; cb[r][3 % VPL] = pk.y >> 16;
+            } else {
+              const unsigned pk = *reinterpret_cast<const unsigned*>(rp);
+              cb[r][0] = pk & 0xffffu; cb[r][1 % VPL] = pk >> 16;
+            }
+#pragma unroll
+            for (int j = 0; j < VPL; ++j) {
+              cmn = cb[r][j] < cmn ? cb[r][j] : cmn;
+              cmax_run = cb[r][j] > cmax_run ? cb[r][j] : cmax_run;
+            }
+          }
+          if (!__any_sync(FULL, cmn == 0u)) {
+            int hb[RB][VPL], inc[RB];
+#pragma unroll
+            for (int r = 0; r < RB; ++r) {
+              hb[r][0] = (int)cb[r][0] - R;
+#pragma unroll
+              for (int j = 1; j < VPL; ++j) hb[r][j] = hb[r][j - 1] + ((int)cb[r][j] - R);
+              inc[r] = hb[r][VPL - 1];
+            }
+#pragma unroll
+            for (int o = 1; o < LPB; o <<= 1) {
+#pragma unroll
+              for (int r = 0; r < RB; ++r) {
+                const int u = __shfl_up_sync(FULL, inc[r], o);
+                if (gl >= o) inc[r] += u;
+              }
+            }
+#pragma unroll
+            for (int r = 0; r < RB; ++r) {
+              const int pvc = inc[r] - hb[r][VPL - 1];  // exclusive lane carry
+              int ep[VPL];
+              if (ND == 3) {
+                if (VPL == 4) {
+                  const int4 p4 = *reinterpret_cast<const int4*>(pp);
+                  ep[0] = p4.x; ep[1 % VPL] = p4.y; ep[2 % VPL] = p4.z; ep[3 % VPL] = p4.w;
+                } else {
+                  const int2 p2 = *reinterpret_cast<const int2*>(pp);
+                  ep[0] = p2.x; ep[1 % VPL] = p2.y;
+                }
+              } else {
+#pragma unroll
+                for (int j = 0; j < VPL; ++j) ep[j] = 0;
+              }
+              float o[VPL];
+              int dv[VPL];
+#pragma unroll
+              for (int j = 0; j < VPL; ++j) {
+                const int gv = hb[r][j] + grow[j] + pvc;
+                grow[j] = gv;
+                dv[j] = gv + ep[j];
+                const double dd = __dadd_rn(__hiloint2double(0x43300000, dv[j] ^ (int)0x80000000),
+                                            -4503601774854144.0);
+                o[j] = __double2float_rn(__dmul_rn(dd, a.q.twoeb));
+                dmax = max(dmax, dv[j]);
+                dmin = min(dmin, dv[j]);
+              }
+              if (ND == 3) {
+                if (VPL == 4) *reinterpret_cast<int4*>(pp) = make_int4(dv[0], dv[1 % VPL], dv[2 % VPL], dv[3 % VPL]);
+                else *reinterpret_cast<int2*>(pp) = make_int2(dv[0], dv[1 % VPL]);
+              }
+              pp += W;
+              if (VPL == 4) *reinterpret_cast<float4*>(dst) = make_float4(o[0], o[1 % VPL], o[2 % VPL], o[3 % VPL]);
+              else *reinterpret_cast<float2*>(dst) = make_float2(o[0], o[1 % VPL]);
+              dst += g.D2;
+            }
+            slot += RB * 32 * F::LANE_BYTES;
+            yl += RB - 1;
+            continue;
+          }
+        }
+#endif
       }
       unsigned c[VPL];
       const unsigned char* rowp = slot;
