@@ -412,10 +412,19 @@ def run_ours(args):
     from paper_2201_04614_b200 import model as M
 
     ws, rank, local = dist_env()
+    # test-only knobs (tests/test_gpu_bench_ranks.py): every rank on cuda:0
+    # with gloo collectives, to run the N-rank path on a one-GPU box (the
+    # ranks' kernels never wait on one another; only timing is meaningless)
+    one_dev = os.environ.get("VLZ_BENCH_ONE_DEVICE") == "1"
+    if one_dev:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if one_dev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     lib = _lib.load()
 
     D0 = args.planes
