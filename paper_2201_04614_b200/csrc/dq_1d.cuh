@@ -18,9 +18,9 @@
 //               sentinels reset it to the verbatim value's prequantized d
 //               (reconstruct.py:30-71), exact fp64 dequantization.
 //
-// Rows whose values leave the int32-exact range (|d| >= 2^30) are handed to
-// the int64 generic kernels through the redo list, by the generic tiles that
-// cover the row (W = 32 * vpl_for(1, b) elements each).
+// Rows whose values leave the int32-exact range (|d| >= 2^30) are redone in
+// int64 by the same warp after its loop, as the generic tiles that cover the
+// row (W = 32 * vpl_for(1, b) elements each).
 #pragma once
 
 #include <type_traits>
@@ -49,8 +49,6 @@ __host__ __device__ constexpr int d1_generic_w() {
 struct D1Args {
   CompressArgs c;
   DecompressArgs d;
-  unsigned int* redo_count;
-  long long* redo_list;
   int meta_smem;  // decompress: per-block counts/offsets/scalars also streamed by the ring
 };
 
@@ -90,15 +88,21 @@ struct D1Ring {
   }
 };
 
-// queue the generic tiles that cover row [e0, e0 + 256) for the int64 redo
+// queue the generic tiles that cover row [e0, e0 + 256) for the warp's int64
+// redo after its loop (slot k of warp `first` is list[k * nwarps + first])
 template <int B>
-__device__ __forceinline__ void d1_redo_row(unsigned int* count, long long* list, int64_t e0,
-                                            int64_t ntiles_generic, int lane) {
+__device__ __forceinline__ void d1_redo_row(uint32_t* nfail_s, long long* list, uint32_t first,
+                                            uint32_t nwarps, int64_t e0, int64_t ntiles_generic,
+                                            int lane) {
   constexpr int WG = d1_generic_w<B>();
   constexpr int PER = D1_ROW / WG;  // 1 or 2
-  if (lane < PER) {
-    const int64_t t = e0 / WG + lane;
-    if (t < ntiles_generic) list[atomicAdd(count, 1u)] = t;
+  if (lane == 0) {
+    uint32_t k = *nfail_s;
+    for (int i = 0; i < PER; ++i) {
+      const int64_t t = e0 / WG + i;
+      if (t < ntiles_generic) list[(size_t)(k++) * nwarps + first] = t;
+    }
+    *nfail_s = k;
   }
 }
 
@@ -124,14 +128,17 @@ __global__ void __launch_bounds__(D1_WARPS * 32, 4)
   D1Ring rg{smem_d1c + (size_t)wib * WS,
             reinterpret_cast<uint64_t*>(smem_d1c + (size_t)wib * WS + D1_STAGES * D1_TILE * 4), 0,
             0u};
+  uint32_t* const nfail_s = reinterpret_cast<uint32_t*>(rg.bars + D1_STAGES);  // tiles left for the tail
   if (lane == 0) {
     for (int s = 0; s < D1_STAGES; ++s) mbar_init(&rg.bars[s], 1);
     fence_mbar_init();
+    *nfail_s = 0u;
   }
   __syncwarp();
   const uint32_t nwarps = gridDim.x * D1_WARPS;
   const uint32_t first = blockIdx.x * D1_WARPS + wib;
   for (int s = 0; s < D1_STAGES; ++s) rg.issue<4>(a.in, first + s * nwarps, nfull, s, lane);
+  if (blockIdx.x == 0 && wib == 0) ws_reset_warp(a.init, lane);  // (behind the first loads)
 
   const int xin = (lane * VPL) % B;  // position of element 0 inside its block
   const int gl = lane & (LPB - 1);
@@ -200,6 +207,7 @@ __global__ void __launch_bounds__(D1_WARPS * 32, 4)
             if (bj) badm |= 1u << j;
             if (ovf) {
               const unsigned long long fi = (unsigned long long)(el + j);
+              ws_wait(a.init);
               if (!isfinite(vj)) atomicMin(a.first_nonfinite, fi);
               atomicMin(a.first_overflow, fi);
             }
@@ -207,7 +215,7 @@ __global__ void __launch_bounds__(D1_WARPS * 32, 4)
           }
         }
         if (__any_sync(FULL, wide)) {  // int32 differences could wrap: int64 redo
-          d1_redo_row<B>(fa.redo_count, fa.redo_list, e0, a.g.ntiles, lane);
+          d1_redo_row<B>(nfail_s, a.redo_list, first, nwarps, e0, a.g.ntiles, lane);
           return;
         }
         // ---- Dx inside the block (the block head reads the zero halo)
@@ -340,25 +348,12 @@ __global__ void __launch_bounds__(D1_WARPS * 32, 4)
     }
   }
 
-  if (MODE == MODE_GLOBAL) {
-    long long s = gacc.sum, c = gcnt;
-    int mn = gacc.mn, mx = gacc.mx;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      s += __shfl_xor_sync(FULL, s, o);
-      c += __shfl_xor_sync(FULL, c, o);
-      const int m1 = __shfl_xor_sync(FULL, mn, o);
-      const int m2 = __shfl_xor_sync(FULL, mx, o);
-      mn = m1 < mn ? m1 : mn;
-      mx = m2 > mx ? m2 : mx;
-    }
-    if (lane == 0 && c > 0) {
-      atomicAdd(a.gsum, (unsigned long long)s);
-      atomicAdd(a.gcount, (unsigned long long)c);
-      atomicMin(a.gmin, (long long)mn);
-      atomicMin(a.gnegmax, -(long long)mx);
-    }
-  }
+  if (MODE == MODE_GLOBAL) commit_global_stats(a, gacc.sum, gcnt, gacc.mn, gacc.mx, lane);
+  // tail: rows whose |d| reached 2^30 (usually none) as generic int64 tiles
+  __syncwarp();
+  const uint32_t nfail = *nfail_s;
+  if (nfail)
+    compress_redo_tail<1, B, (B == 256 ? 8 : 4), MODE>(a, first, nwarps, nfail, lane, nullptr);
 }
 
 // -------------------------------------------------------------- decompress
@@ -386,6 +381,9 @@ __global__ void __launch_bounds__(D1_WARPS * 32, VLZ_D1D_MINB)
   D1Ring rg{smem_d1d + (size_t)wib * WS,
             reinterpret_cast<uint64_t*>(smem_d1d + (size_t)wib * WS + D1_STAGES * DS::BYTES), 0,
             0u};
+  // generic tiles left for the int64 tail, per warp (a word of the barrier area)
+  uint32_t* const s_nfail = reinterpret_cast<uint32_t*>(rg.bars + D1_STAGES) - wib;
+  if (lane == 0) s_nfail[wib] = 0u;
   const bool meta = fa.meta_smem != 0;
   const bool scal_blocks = a.mode == MODE_BLOCK || a.mode == MODE_EDGE;
   // one stage: the tile's codes and, with `meta`, its blocks' counts /
@@ -563,7 +561,7 @@ __global__ void __launch_bounds__(D1_WARPS * 32, VLZ_D1D_MINB)
         }
         wide |= dmax >= (1 << 30) || dmin < -(1 << 30);
         if (__any_sync(FULL, wide)) {  // leave the row to the int64 kernel
-          d1_redo_row<B>(fa.redo_count, fa.redo_list, e0, a.g.ntiles, lane);
+          d1_redo_row<B>(&s_nfail[wib], a.redo_list, first, nwarps, e0, a.g.ntiles, lane);
           return;
         }
         if (smask) {
@@ -614,9 +612,12 @@ __global__ void __launch_bounds__(D1_WARPS * 32, VLZ_D1D_MINB)
       rg.parity ^= 1u;
     }
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) sent_acc += __shfl_xor_sync(FULL, sent_acc, o);
-  if (lane == 0 && sent_acc) atomicAdd(a.sentinels, (unsigned long long)sent_acc);
+  // tail: rows outside the int32-exact range (usually none) as generic int64 tiles
+  __syncwarp();
+  const uint32_t nfail = s_nfail[wib];
+  if (nfail)
+    decompress_redo_tail<1, B, (B == 256 ? 8 : 4)>(a, first, nwarps, nfail, lane, nullptr, sent_acc);
+  decompress_finish(a, sent_acc, lane);
 }
 
 }  // namespace vlz

@@ -50,10 +50,32 @@ struct CompressArgs {
   unsigned long long* gcount;
   long long* gmin;
   long long* gnegmax;
-  // int64 redo list written by the fast kernel (tile ids)
-  const unsigned int* redo_count;
-  const long long* redo_list;
+  // failed-tile slots of the fused kernels (tile ids redone in int64 by the
+  // same warp at the end of its loop: slot k of warp w is redo_list[k * nwarps + w])
+  long long* redo_list;
+  InitArgs init;  // per-call reset done by CTA 0 (vlz_common.cuh)
 };
+
+// the warp's global statistics -> the call's accumulators (after the reset)
+__device__ __forceinline__ void commit_global_stats(const CompressArgs& a, long long s, long long c,
+                                                    int mn, int mx, int lane) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(FULL, s, o);
+    c += __shfl_xor_sync(FULL, c, o);
+    const int m1 = __shfl_xor_sync(FULL, mn, o);
+    const int m2 = __shfl_xor_sync(FULL, mx, o);
+    mn = m1 < mn ? m1 : mn;
+    mx = m2 > mx ? m2 : mx;
+  }
+  if (lane == 0 && c > 0) {
+    ws_wait(a.init);
+    atomicAdd(a.gsum, (unsigned long long)s);
+    atomicAdd(a.gcount, (unsigned long long)c);
+    atomicMin(a.gmin, (long long)mn);
+    atomicMin(a.gnegmax, -(long long)mx);
+  }
+}
 
 // per-warp statistics for MODE_GLOBAL (lane partials)
 struct GlobalAcc {
@@ -160,6 +182,7 @@ __device__ __forceinline__ bool compress_tile(const CompressArgs& a, int64_t til
           if (bad) badm |= 1u << j;
           if (ovf) {
             const unsigned long long fi = (unsigned long long)(row + xl0 + j);
+            ws_wait(a.init);
             if (!isfinite(v[j])) atomicMin(a.first_nonfinite, fi);
             atomicMin(a.first_overflow, fi);
           }
@@ -349,50 +372,49 @@ __device__ __forceinline__ bool compress_tile(const CompressArgs& a, int64_t til
   return false;
 }
 
-// LIST = false: every tile (uint32 stencil, int64 redo on demand).
-// LIST = true : only the tiles the fast kernel appended to the redo list,
-//               directly in int64 (dq_compress_fast.cuh).
-template <int ND, int B, int VPL, int MODE, bool LIST = false>
+// Every tile in the uint32 stencil, redone in int64 on demand.
+template <int ND, int B, int VPL, int MODE>
 __global__ void __launch_bounds__(128) dq_compress_kernel(CompressArgs a) {
   pdl_enter();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int PB = plane_smem_bytes<ND, B, VPL>();
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
+  if (blockIdx.x == 0 && wib == 0) ws_reset_warp(a.init, lane);
   unsigned char* wsm = smem_raw + (size_t)wib * PB;
   GlobalAcc gacc;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  const int64_t ntodo = LIST ? (int64_t)*a.redo_count : a.g.ntiles;
-  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib; i < ntodo; i += nwarps) {
-    if (LIST) {
-      compress_tile<ND, B, VPL, MODE, long long>(a, a.redo_list[i], lane,
-                                                 reinterpret_cast<long long*>(wsm), gacc);
-    } else if (compress_tile<ND, B, VPL, MODE, unsigned>(a, i, lane,
-                                                         reinterpret_cast<unsigned*>(wsm), gacc)) {
+  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib; i < a.g.ntiles; i += nwarps) {
+    if (compress_tile<ND, B, VPL, MODE, unsigned>(a, i, lane, reinterpret_cast<unsigned*>(wsm),
+                                                  gacc)) {
       compress_tile<ND, B, VPL, MODE, long long>(a, i, lane,
                                                  reinterpret_cast<long long*>(wsm), gacc);
     }
   }
-  if (MODE == MODE_GLOBAL) {
-    // warp reduce, then one atomic set per warp
-    long long s = gacc.sum, c = gacc.cnt;
-    int mn = gacc.mn, mx = gacc.mx;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      s += __shfl_xor_sync(FULL, s, o);
-      c += __shfl_xor_sync(FULL, c, o);
-      const int m1 = __shfl_xor_sync(FULL, mn, o);
-      const int m2 = __shfl_xor_sync(FULL, mx, o);
-      mn = m1 < mn ? m1 : mn;
-      mx = m2 > mx ? m2 : mx;
-    }
-    if (lane == 0 && c > 0) {
-      atomicAdd(a.gsum, (unsigned long long)s);
-      atomicAdd(a.gcount, (unsigned long long)c);
-      atomicMin(a.gmin, (long long)mn);
-      atomicMin(a.gnegmax, -(long long)mx);
-    }
-  }
+  if (MODE == MODE_GLOBAL) commit_global_stats(a, gacc.sum, gacc.cnt, gacc.mn, gacc.mx, lane);
+}
+
+// int64 redo of the tiles a fused kernel's warp could not finish in int32
+// (slot k of warp `first` is redo_list[k * nwarps + first]); kept out of line
+// so that the fused kernels' register allocation is that of their hot loops
+#ifndef VLZ_TAIL_MODE
+#define VLZ_TAIL_MODE 2  // 2: inlined (C5 fused compress: neutral; 1, out of line: +1.7 %);
+                         // 0: absent (timing experiments only)
+#endif
+#if VLZ_TAIL_MODE == 2
+#define VLZ_TAIL_ATTR __forceinline__
+#else
+#define VLZ_TAIL_ATTR __noinline__
+#endif
+template <int ND, int B, int VPL, int MODE>
+__device__ VLZ_TAIL_ATTR void compress_redo_tail(const CompressArgs& a, uint32_t first,
+                                                uint32_t nwarps, uint32_t nfail, int lane,
+                                                long long* plane_smem) {
+  GlobalAcc gacc;
+  for (uint32_t k = 0; k < nfail; ++k)
+    compress_tile<ND, B, VPL, MODE, long long>(a, a.redo_list[(size_t)k * nwarps + first], lane,
+                                               plane_smem, gacc);
+  if (MODE == MODE_GLOBAL) commit_global_stats(a, gacc.sum, gacc.cnt, gacc.mn, gacc.mx, lane);
 }
 
 }  // namespace vlz

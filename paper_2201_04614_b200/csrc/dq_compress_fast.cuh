@@ -11,8 +11,8 @@
 //  * prequantization runs the float32 fast path (vlz_common.cuh quant_fast)
 //    and re-evaluates only flagged elements with the exact float64 rules;
 //  * the Lorenzo stencil runs in int32 (every |d| of the tile < 2^24); a tile
-//    holding a larger |d| is appended to a redo list and recomputed in int64 by
-//    dq_compress_kernel<..., LIST=true>; such a tile commits nothing here;
+//    holding a larger |d| commits nothing in the streamed pass and is redone in
+//    int64 by the same warp after its loop (compress_redo_tail: no redo launch);
 //  * interior tiles (whole window inside the row, full block rows) take a
 //    branch-free specialisation with constant code strides;
 //  * tile ids are decoded with 32-bit magic division, ring slots advance
@@ -113,8 +113,6 @@ __host__ __device__ constexpr int fast_smem_bytes() {
 struct FastArgs {
   CUtensorMap tmap;  // input viewed as (D2, D1, D0) uint32, box (W, BY, 1)
   CompressArgs c;
-  unsigned int* redo_count;
-  long long* redo_list;
 };
 
 struct TileXY {
@@ -213,7 +211,8 @@ template <int ND, int B, int VPL, int MODE, int K, bool INTERIOR>
 __device__ __forceinline__ void fast_tile(const FastArgs& fa, uint32_t tile, const TileXY& tc,
                                           int lane, float* ring, uint64_t* bars,
                                           Producer<ND, B, VPL>& prod, Consumer<ND, B, VPL>& cons,
-                                          uint32_t nwarps, KAcc<K>& gacc, long long& gcnt) {
+                                          uint32_t nwarps, KAcc<K>& gacc, long long& gcnt,
+                                          uint32_t* nfail_s) {
   using S = Shape<ND, B, VPL>;
   using F = FastShape<ND, B, VPL>;
   constexpr int BZ = S::BZ, BY = S::BY, BX = S::BX, W = S::W, LPB = S::LPB;
@@ -482,6 +481,7 @@ __device__ __forceinline__ void fast_tile(const FastArgs& fa, uint32_t tile, con
           if (ovf) {
             const unsigned long long fi =
                 (unsigned long long)(((z0 + zl) * g.D1 + (y0 + yl)) * g.D2 + xl0 + j);
+            ws_wait(a.init);
             if (!isfinite(vj)) atomicMin(a.first_nonfinite, fi);
             atomicMin(a.first_overflow, fi);
           }
@@ -634,9 +634,14 @@ __device__ __forceinline__ void fast_tile(const FastArgs& fa, uint32_t tile, con
     if (MODE == MODE_GLOBAL) tcnt += (long long)nvalid * ey;
   }
 
-  // int32 stencil may have wrapped: hand the whole tile to the int64 redo
+  // int32 stencil may have wrapped: the warp redoes the whole tile in int64
+  // after its loop (slot k of this warp; the kernel's tail)
   if (__any_sync(FULL, wide)) {
-    if (lane == 0) fa.redo_list[atomicAdd(fa.redo_count, 1u)] = tile;
+    if (lane == 0) {
+      const uint32_t k = *nfail_s;
+      a.redo_list[(size_t)k * nwarps + tile % nwarps] = tile;
+      *nfail_s = k + 1;
+    }
     return;
   }
 
@@ -702,9 +707,11 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, (FastShape<ND, B, VPL>::MINB)
                                                FAST_STAGES * F::STAGE_BYTES + F::PREV_BYTES);
   const Geo& g = fa.c.g;
 
+  uint32_t* const nfail_s = reinterpret_cast<uint32_t*>(bars + FAST_STAGES);  // tiles left for the tail
   if (lane == 0) {
     for (int s = 0; s < FAST_STAGES; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
+    *nfail_s = 0u;
   }
   __syncwarp();
 
@@ -714,6 +721,7 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, (FastShape<ND, B, VPL>::MINB)
   Producer<ND, B, VPL> prod;
   prod.start(g, first);
   for (int s = 0; s < FAST_STAGES; ++s) prod.issue(g, &fa.tmap, ring, bars, lane, nwarps);
+  if (blockIdx.x == 0 && wib == 0) ws_reset_warp(fa.c.init, lane);  // (behind the first loads)
   Consumer<ND, B, VPL> cons{0, 0u};
   KAcc<K> gacc;
   long long gcnt = 0;
@@ -724,31 +732,35 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, (FastShape<ND, B, VPL>::MINB)
                           ((int64_t)(tc.by + 1) * S::BY <= g.D1);
     if (interior)
       fast_tile<ND, B, VPL, MODE, K, true>(fa, tile, tc, lane, ring, bars, prod, cons, nwarps,
-                                           gacc, gcnt);
+                                           gacc, gcnt, nfail_s);
     else
       fast_tile<ND, B, VPL, MODE, K, false>(fa, tile, tc, lane, ring, bars, prod, cons, nwarps,
-                                            gacc, gcnt);
+                                            gacc, gcnt, nfail_s);
   }
 
-  if (MODE == MODE_GLOBAL) {
-    const CompressArgs& a = fa.c;
-    long long s = gacc.sum, c = gcnt;
-    int mn = gacc.mn, mx = gacc.mx;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      s += __shfl_xor_sync(FULL, s, o);
-      c += __shfl_xor_sync(FULL, c, o);
-      const int m1 = __shfl_xor_sync(FULL, mn, o);
-      const int m2 = __shfl_xor_sync(FULL, mx, o);
-      mn = m1 < mn ? m1 : mn;
-      mx = m2 > mx ? m2 : mx;
+  if (MODE == MODE_GLOBAL) commit_global_stats(fa.c, gacc.sum, gcnt, gacc.mn, gacc.mx, lane);
+
+  // tail: tiles whose |d| reached 2^24 (usually none), redone in int64 by the
+  // warp that met them.  Shapes whose int64 plane lives in shared memory take
+  // turns on the CTA's whole allocation (all rings are idle by then).
+  __syncwarp();
+#if VLZ_TAIL_MODE == 0
+  const uint32_t nfail = 0u;
+#else
+  const uint32_t nfail = *nfail_s;
+#endif
+  if constexpr (S::PLANE_SMEM) {
+    static_assert(fast_smem_bytes<ND, B, VPL>() >= plane_smem_bytes<ND, B, VPL>(), "tail plane");
+    if (__syncthreads_or(nfail != 0u)) {
+      for (int w = 0; w < FAST_WARPS; ++w) {
+        if (w == wib && nfail)
+          compress_redo_tail<ND, B, VPL, MODE>(fa.c, first, nwarps, nfail, lane,
+                                               reinterpret_cast<long long*>(smem_fast));
+        __syncthreads();
+      }
     }
-    if (lane == 0 && c > 0) {
-      atomicAdd(a.gsum, (unsigned long long)s);
-      atomicAdd(a.gcount, (unsigned long long)c);
-      atomicMin(a.gmin, (long long)mn);
-      atomicMin(a.gnegmax, -(long long)mx);
-    }
+  } else if (nfail) {
+    compress_redo_tail<ND, B, VPL, MODE>(fa.c, first, nwarps, nfail, lane, nullptr);
   }
 }
 

@@ -44,8 +44,10 @@ struct DecompressArgs {
   int* status;
   long long* index;
   long long* n_sent_out;
-  const unsigned int* redo_count;  // tiles queued by the fast kernel
-  const long long* redo_list;
+  // failed-tile slots of the fused kernels (redone in int64 by the same warp
+  // after its loop: slot k of warp w is redo_list[k * nwarps + w])
+  long long* redo_list;
+  unsigned long long* flag;  // the call's reset flag, cleared by the last CTA
 };
 
 // the stream's outlier count: a host value, or a device word written by an
@@ -267,27 +269,19 @@ __device__ __forceinline__ void decompress_tile(const DecompressArgs& a, int64_t
   }
 }
 
-// LIST = true: only the tiles queued by dq_decompress_fast_kernel (edge tiles
-// and tiles that failed the int32 exactness check), in int64 as always.
-template <int ND, int B, int VPL, typename CT, bool LIST = false>
-__global__ void __launch_bounds__(128) dq_decompress_kernel(DecompressArgs a) {
-  pdl_enter();
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  constexpr int PB = plane_smem_bytes<ND, B, VPL>();
-  const int lane = threadIdx.x & 31;
-  const int wib = threadIdx.x >> 5;
-  long long* wsm = reinterpret_cast<long long*>(smem_raw + (size_t)wib * PB);
-  long long sent = 0;
-  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  const int64_t ntodo = LIST ? (int64_t)*a.redo_count : a.g.ntiles;
-  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib; i < ntodo; i += nwarps)
-    decompress_tile<ND, B, VPL, CT>(a, LIST ? a.redo_list[i] : i, lane, wsm, sent);
+// End of every decompress kernel (all threads of the CTA): the warp's sentinel
+// count joins the total, and the last CTA to finish turns the per-block
+// findings into the reference's error order: sentinel total vs stored outliers
+// first (reconstruct.py:87-91), then the first failing block
+// (reconstruct.py:43-66, sequential block order).
+__device__ __forceinline__ void decompress_finish(const DecompressArgs& a, long long sent,
+                                                  int lane) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) sent += __shfl_xor_sync(FULL, sent, o);
   if (lane == 0 && sent) atomicAdd(a.sentinels, (unsigned long long)sent);
-  // last CTA turns the per-block findings into the reference's error order:
-  // sentinel total vs stored outliers first (reconstruct.py:87-91), then the
-  // first failing block (reconstruct.py:43-66, sequential block order)
+#ifdef VLZ_NO_DFINISH  // (timing experiments only)
+  return;
+#endif
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
@@ -296,6 +290,7 @@ __global__ void __launch_bounds__(128) dq_decompress_kernel(DecompressArgs a) {
       __threadfence();
       const unsigned long long ns = atomicAdd(a.sentinels, 0ull);
       const unsigned long long fb = atomicAdd(a.first_bad, 0ull);
+      *a.flag = 0ull;  // a graph replay of this call starts from a cleared flag
       *a.n_sent_out = (long long)ns;
       if ((long long)ns != n_outliers_of(a)) {
         *a.status = 7;  // VLZ_ST_SENTINEL_TOTAL
@@ -306,6 +301,42 @@ __global__ void __launch_bounds__(128) dq_decompress_kernel(DecompressArgs a) {
       }
     }
   }
+}
+
+// int64 redo of the tiles a fused kernel's warp could not finish in int32
+// (slot k of warp `first` is redo_list[k * nwarps + first]); out of line so
+// that the fused kernels keep the register allocation of their hot loops
+#ifndef VLZ_DTAIL_MODE
+#define VLZ_DTAIL_MODE 1  // 1: out of line; 2: inlined
+#endif
+#if VLZ_DTAIL_MODE == 2
+#define VLZ_DTAIL_ATTR __forceinline__
+#else
+#define VLZ_DTAIL_ATTR __noinline__
+#endif
+template <int ND, int B, int VPL>
+__device__ VLZ_DTAIL_ATTR void decompress_redo_tail(const DecompressArgs& a, uint32_t first,
+                                                  uint32_t nwarps, uint32_t nfail, int lane,
+                                                  long long* plane_smem, long long& sent) {
+  for (uint32_t k = 0; k < nfail; ++k)
+    decompress_tile<ND, B, VPL, uint16_t>(a, a.redo_list[(size_t)k * nwarps + first], lane,
+                                          plane_smem, sent);
+}
+
+// every tile in int64 (shapes and code widths without a fused kernel)
+template <int ND, int B, int VPL, typename CT>
+__global__ void __launch_bounds__(128) dq_decompress_kernel(DecompressArgs a) {
+  pdl_enter();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int PB = plane_smem_bytes<ND, B, VPL>();
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  long long* wsm = reinterpret_cast<long long*>(smem_raw + (size_t)wib * PB);
+  long long sent = 0;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib; i < a.g.ntiles; i += nwarps)
+    decompress_tile<ND, B, VPL, CT>(a, i, lane, wsm, sent);
+  decompress_finish(a, sent, lane);
 }
 
 }  // namespace vlz

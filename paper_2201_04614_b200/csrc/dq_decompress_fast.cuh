@@ -47,7 +47,10 @@ namespace vlz {
 #endif
 
 // ring depth of the decompress producers (planes in flight per warp)
-constexpr int DSTAGES = 2;
+#ifndef VLZ_DSTAGES
+#define VLZ_DSTAGES 2
+#endif
+constexpr int DSTAGES = VLZ_DSTAGES;
 
 template <int ND, int B, int VPL>
 struct DFastShape {
@@ -80,8 +83,6 @@ __host__ __device__ constexpr int dfast_smem_bytes() {
 struct DFastArgs {
   CUtensorMap tmap;  // TMA path: codes as (64, BZ, nblocks) uint16, box (64, 1, NBLK)
   DecompressArgs d;
-  unsigned int* redo_count;
-  long long* redo_list;
 };
 
 template <int ND, int B, int VPL>
@@ -201,7 +202,8 @@ template <int ND, int B, int VPL, bool EDGE, class Prod>
 __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, const TileXY& tc,
                                            int lane, unsigned char* ring, uint64_t* bars,
                                            Prod& prod, Consumer<ND, B, VPL, DSTAGES>& cons,
-                                           uint32_t nwarps, long long& sent_acc) {
+                                           uint32_t nwarps, long long& sent_acc,
+                                           uint32_t* nfail_s) {
   constexpr bool TMAP = Prod::TMAP;
   using S = Shape<ND, B, VPL>;
   using F = DFastShape<ND, B, VPL>;
@@ -575,7 +577,11 @@ __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, c
   }
   wide |= dmax >= (1 << 27) || dmin < -(1 << 27);
   if (__any_sync(FULL, wide)) {
-    if (lane == 0) fa.redo_list[atomicAdd(fa.redo_count, 1u)] = tile;
+    if (lane == 0) {  // slot k of this warp: redone in int64 after the loop
+      const uint32_t k = *nfail_s;
+      a.redo_list[(size_t)k * nwarps + tile % nwarps] = tile;
+      *nfail_s = k + 1;
+    }
     return;
   }
   const bool bad_any = group_any<LPB>(cmax_run >= (unsigned)(2 * R), lane);
@@ -593,7 +599,8 @@ __device__ __forceinline__ void dfast_tile(const DFastArgs& fa, uint32_t tile, c
 // registers of a second instantiation of the tile body); grids without them
 // take the lean variant
 template <int ND, int B, int VPL, bool EDGES>
-__global__ void __launch_bounds__(FAST_WARPS * 32, (EDGES && B == 8) ? 3 : 4)
+__global__ void __launch_bounds__(FAST_WARPS * 32,
+                                  ((EDGES && B == 8) || (ND == 3 && (B == 16 || B == 64))) ? 3 : 4)
     dq_decompress_fast_kernel(const __grid_constant__ DFastArgs fa) {
   pdl_enter();
   using F = DFastShape<ND, B, VPL>;
@@ -601,6 +608,14 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, (EDGES && B == 8) ? 3 : 4)
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   unsigned char* ring = smem_dfast + (size_t)wib * F::warp_smem(EDGES);
+  // tiles left for the int64 tail of this warp: a register (a static shared
+  // array would push 3 CTAs of the b = 16 shape past the 196 KB carve-out step
+  // and halve their L1: C4 b=16 decompress 178 -> 199 us)
+  uint32_t nfail_reg = 0u;
+  uint32_t* const s_nfail = &nfail_reg - wib;
+  static_assert(!Shape<ND, B, VPL>::PLANE_SMEM ||
+                    dfast_smem_bytes<ND, B, VPL, false>() >= plane_smem_bytes<ND, B, VPL>(),
+                "tail plane");
   const Geo& g = fa.d.g;
   const uint16_t* codes = reinterpret_cast<const uint16_t*>(fa.d.codes);
 
@@ -614,13 +629,32 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, (EDGES && B == 8) ? 3 : 4)
   for (uint32_t tile = first; tile < (uint32_t)g.ntiles; tile += nwarps) {
     const TileXY tc = decode_tile(g, tile);
     if (tile_interior<ND, B, VPL>(g, tc))
-      dfast_tile<ND, B, VPL, false>(fa, tile, tc, lane, ring, nullptr, prod, cons, nwarps, sent);
+      dfast_tile<ND, B, VPL, false>(fa, tile, tc, lane, ring, nullptr, prod, cons, nwarps, sent, &s_nfail[wib]);
     else if constexpr (EDGES)  // same recurrence, synchronous fill (the ring keeps streaming)
-      dfast_tile<ND, B, VPL, true>(fa, tile, tc, lane, ring, nullptr, prod, cons, nwarps, sent);
+      dfast_tile<ND, B, VPL, true>(fa, tile, tc, lane, ring, nullptr, prod, cons, nwarps, sent, &s_nfail[wib]);
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) sent += __shfl_xor_sync(FULL, sent, o);
-  if (lane == 0 && sent) atomicAdd(fa.d.sentinels, (unsigned long long)sent);
+  // tail: tiles outside the int32-exact range (usually none), redone in int64
+  // by the warp that met them; shapes whose int64 plane lives in shared memory
+  // take turns on the CTA's whole allocation (every ring is idle by then)
+  __syncwarp();
+#if VLZ_DTAIL_MODE == 0
+  const uint32_t nfail = 0u;
+#else
+  const uint32_t nfail = __shfl_sync(FULL, s_nfail[wib], 0);  // (lane 0 keeps the count)
+#endif
+  if constexpr (Shape<ND, B, VPL>::PLANE_SMEM) {
+    if (__syncthreads_or(nfail != 0u)) {
+      for (int w = 0; w < FAST_WARPS; ++w) {
+        if (w == wib && nfail)
+          decompress_redo_tail<ND, B, VPL>(fa.d, first, nwarps, nfail, lane,
+                                           reinterpret_cast<long long*>(smem_dfast), sent);
+        __syncthreads();
+      }
+    }
+  } else if (nfail) {
+    decompress_redo_tail<ND, B, VPL>(fa.d, first, nwarps, nfail, lane, nullptr, sent);
+  }
+  decompress_finish(fa.d, sent, lane);
 }
 
 // TMA variant (DTProducer): per-warp [stages | previous plane | barriers],
@@ -652,6 +686,10 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, EDGES ? 3 : VLZ_DTMA_MINB)
   const int wib = threadIdx.x >> 5;
   unsigned char* ring = base + (size_t)wib * T::WARP_SMEM;
   uint64_t* bars = reinterpret_cast<uint64_t*>(ring + T::BAR_OFF);
+  // tiles left for the int64 tail, per warp (a word of the barrier area: a
+  // static array would pad the 1024-byte aligned dynamic allocation by 1 KB)
+  uint32_t* const s_nfail = reinterpret_cast<uint32_t*>(bars + DSTAGES) - wib;
+  if (lane == 0) s_nfail[wib] = 0u;
   const Geo& g = fa.d.g;
   if (lane == 0) {
     for (int s = 0; s < DSTAGES; ++s) mbar_init(&bars[s], 1);
@@ -670,13 +708,32 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, EDGES ? 3 : VLZ_DTMA_MINB)
   for (uint32_t tile = first; tile < (uint32_t)g.ntiles; tile += nwarps) {
     const TileXY tc = decode_tile(g, tile);
     if (tile_interior<ND, B, VPL>(g, tc))
-      dfast_tile<ND, B, VPL, false>(fa, tile, tc, lane, ring, bars, prod, cons, nwarps, sent);
+      dfast_tile<ND, B, VPL, false>(fa, tile, tc, lane, ring, bars, prod, cons, nwarps, sent, &s_nfail[wib]);
     else if constexpr (EDGES)
-      dfast_tile<ND, B, VPL, true>(fa, tile, tc, lane, ring, bars, prod, cons, nwarps, sent);
+      dfast_tile<ND, B, VPL, true>(fa, tile, tc, lane, ring, bars, prod, cons, nwarps, sent, &s_nfail[wib]);
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) sent += __shfl_xor_sync(FULL, sent, o);
-  if (lane == 0 && sent) atomicAdd(fa.d.sentinels, (unsigned long long)sent);
+  // tail: tiles outside the int32-exact range (usually none), redone in int64
+  // by the warp that met them; shapes whose int64 plane lives in shared memory
+  // take turns on the CTA's whole allocation (every ring is idle by then)
+  __syncwarp();
+#if VLZ_DTAIL_MODE == 0
+  const uint32_t nfail = 0u;
+#else
+  const uint32_t nfail = __shfl_sync(FULL, s_nfail[wib], 0);  // (lane 0 keeps the count)
+#endif
+  if constexpr (Shape<ND, B, VPL>::PLANE_SMEM) {
+    if (__syncthreads_or(nfail != 0u)) {
+      for (int w = 0; w < FAST_WARPS; ++w) {
+        if (w == wib && nfail)
+          decompress_redo_tail<ND, B, VPL>(fa.d, first, nwarps, nfail, lane,
+                                           reinterpret_cast<long long*>(base), sent);
+        __syncthreads();
+      }
+    }
+  } else if (nfail) {
+    decompress_redo_tail<ND, B, VPL>(fa.d, first, nwarps, nfail, lane, nullptr, sent);
+  }
+  decompress_finish(fa.d, sent, lane);
 }
 
 // edge tiles: the last window of every block row when W does not divide D2,

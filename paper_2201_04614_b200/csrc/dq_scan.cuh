@@ -56,6 +56,8 @@ struct ScanArgs {
   int64_t* scalars;
   unsigned long long* lb;  // per chunk look-back words
   unsigned int* ticket;
+  unsigned long long* flag;  // compress: the call's reset flag, cleared at the end
+  InitArgs init;             // decompress: reset done by CTA 0 of the offsets kernel
   long long* n_out;
   const long long* gstats;  // sum, count, min, neg_max per record (nstats records:
   int nstats;               // one reduced record, or one per rank when sharded)
@@ -343,6 +345,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) dq_scan_kernel(ScanArgs a) {
   // 3. look-back, then the compact stores
   const long long cexcl = lookback_cta(a.lb, tile, agg, s_first, s_wsum);
   if (tid == 0 && base + SCAN_CH >= nb) {
+    *a.flag = 0ull;  // a graph replay of this call starts from a cleared flag
     *a.n_out = cexcl + agg;
     if (fix && a.scalars) a.scalars[0] = s0;
     if (a.status) {
@@ -433,11 +436,14 @@ __global__ void __launch_bounds__(SCAN_THREADS) dq_offsets_kernel(ScanArgs a, in
   __shared__ long long s_warp[SCAN_THREADS / 32];
   __shared__ int s_first[SCAN_THREADS / 32];
   __shared__ long long s_wsum[SCAN_THREADS / 32];
-  __shared__ unsigned int s_tile;
   const int tid = threadIdx.x;
-  if (tid == 0) s_tile = atomicAdd(a.ticket, 1u);
-  __syncthreads();
-  const int64_t tile = s_tile;
+  // first kernel of a decompress call: CTA 0 resets the result block, the
+  // header and the look-back words (no init launch).  Ranges go by blockIdx
+  // (at most ~4 CTAs per SM exist, all resident or dispatched in index order,
+  // so every predecessor of a waiting CTA is running); the look-back words are
+  // first touched after the range sum, behind the reset flag.
+  if (blockIdx.x == 0) ws_reset_cta0(a.init);
+  const int64_t tile = blockIdx.x;
   const int64_t nb = a.g.nblocks;
   const int64_t lo = tile * span;
   const int64_t hi = lo + span < nb ? lo + span : nb;
@@ -456,6 +462,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) dq_offsets_kernel(ScanArgs a, in
     for (int k = 0; k < OFF_IPT; ++k) part += v[k];
   }
   long long agg;
+  if (tid == 0) ws_wait(a.init);  // (ordered before the other threads' look-back reads by the scan's barrier)
   cta_excl_scan<long long>(part, s_warp, agg);
   publish_aggregate(a.lb, tile, agg);
   // first sweep of the second pass in flight during the look-back

@@ -1,4 +1,4 @@
-// k_1d.cu -- launch of the fused 1-D kernels (dq_1d.cuh) + their int64 redo.
+// k_1d.cu -- launch of the fused 1-D kernels (dq_1d.cuh).
 #include "dq_1d.cuh"
 #include "launch.cuh"
 
@@ -23,8 +23,6 @@ template <int B, int MODE, int K>
 static cudaError_t run_c1d(const CompressArgs& a, cudaStream_t st) {
   D1Args fa{};
   fa.c = a;
-  fa.redo_count = const_cast<unsigned int*>(a.redo_count);
-  fa.redo_list = const_cast<long long*>(a.redo_list);
   auto kern = dq_compress_1d_kernel<B, MODE, K>;
   constexpr int smem = D1_WARPS * d1_warp_smem<4>();
   int64_t grid = 0;
@@ -35,17 +33,6 @@ static cudaError_t run_c1d(const CompressArgs& a, cudaStream_t st) {
   e = launch_k(kern, (unsigned)grid, D1_WARPS * 32, smem, st, fa);
   if (e != cudaSuccess) return e;
   if (t) timing_mark(TK_COMPRESS, false, st);
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  // int64 redo of the rows whose |d| reached 2^30 (usually none: exits at once)
-  constexpr int VG = B == 256 ? 8 : 4;
-  auto redo = dq_compress_kernel<1, B, VG, MODE, true>;
-  constexpr int psmem = 4 * plane_smem_bytes<1, B, VG>();
-  if (t) timing_mark(TK_REDO, true, st);
-  e = launch_k(redo, (unsigned)num_sms(), 128, psmem, st, a);
-  if (e != cudaSuccess) return e;
-  if (t) timing_mark(TK_REDO, false, st);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
@@ -68,8 +55,8 @@ static cudaError_t run_c1d_b(int mode, const CompressArgs& a, cudaStream_t st) {
   }
 }
 
-// below ~4 M elements the call is launch bound: one generic kernel beats the
-// fused kernel + its (usually empty) int64 redo launch
+// arrays below this many elements take the generic kernel (VLZ_D1_MIN_N
+// overrides it for A/B runs)
 static int64_t d1_min_n() {
   static const int64_t v = [] {
     const char* e = std::getenv("VLZ_D1_MIN_N");  // A/B runs of the threshold
@@ -99,8 +86,6 @@ template <int B>
 static cudaError_t run_d1d(const DecompressArgs& a, cudaStream_t st) {
   D1Args fa{};
   fa.d = a;
-  fa.redo_count = const_cast<unsigned int*>(a.redo_count);
-  fa.redo_list = const_cast<long long*>(a.redo_list);
   // the ring also streams counts / offsets / block scalars when aligned
   const bool scal = a.mode == MODE_BLOCK || a.mode == MODE_EDGE;
   fa.meta_smem = ((reinterpret_cast<uintptr_t>(a.counts) & 15) == 0) &&
@@ -116,17 +101,6 @@ static cudaError_t run_d1d(const DecompressArgs& a, cudaStream_t st) {
   e = launch_k(kern, (unsigned)grid, D1_WARPS * 32, smem, st, fa);
   if (e != cudaSuccess) return e;
   if (t) timing_mark(TK_DECOMPRESS, false, st);
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  // int64 redo of flagged rows; its last CTA also settles the status
-  constexpr int VG = B == 256 ? 8 : 4;
-  auto redo = dq_decompress_kernel<1, B, VG, uint16_t, true>;
-  constexpr int psmem = 4 * plane_smem_bytes<1, B, VG>();
-  if (t) timing_mark(TK_REDO, true, st);
-  e = launch_k(redo, (unsigned)num_sms() * 2, 128, psmem, st, a);
-  if (e != cudaSuccess) return e;
-  if (t) timing_mark(TK_REDO, false, st);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }

@@ -1,7 +1,7 @@
 // k_decompress.cu -- reconstruction kernel instantiations and dispatch.
 //   fast shapes (3-D b=8/16, 2-D b=8/16), uint16 codes, aligned buffers:
-//       dq_decompress_fast_kernel (interior tiles, int32 with exactness check)
-//       + dq_decompress_kernel<LIST> (flagged tiles, int64)
+//       dq_decompress_fast_kernel (int32 with exactness check; its warps redo
+//       flagged tiles in int64 themselves and the last CTA settles the status)
 //   everything else: dq_decompress_kernel (int64)
 #include "dq_decompress_fast.cuh"
 #include "launch.cuh"
@@ -40,8 +40,6 @@ static cudaError_t run_d(bool u32, const DecompressArgs& a, cudaStream_t st) {
     if (aligned) {
       DFastArgs fa{};
       fa.d = a;
-      fa.redo_count = const_cast<unsigned int*>(a.redo_count);
-      fa.redo_list = const_cast<long long*>(a.redo_list);
       const bool edges = edge_tile_count<ND, B, VPL>(a.g) > 0;
       auto kern = edges ? dq_decompress_fast_kernel<ND, B, VPL, true>
                         : dq_decompress_fast_kernel<ND, B, VPL, false>;
@@ -68,19 +66,6 @@ static cudaError_t run_d(bool u32, const DecompressArgs& a, cudaStream_t st) {
       e = launch_k(kern, (unsigned)grid, FAST_WARPS * 32, fsmem, st, fa);
       if (e != cudaSuccess) return e;
       if (t) timing_mark(TK_DECOMPRESS, false, st);
-      g_launches.fetch_add(1, std::memory_order_relaxed);
-      e = cudaGetLastError();
-      if (e != cudaSuccess) return e;
-      auto redo = dq_decompress_kernel<ND, B, VPL, uint16_t, true>;
-      if (smem > 48 * 1024) {
-        int rps = 0;
-        e = occupancy(redo, 128, smem, rps);  // (its smem opt-in, once)
-        if (e != cudaSuccess) return e;
-      }
-      if (t) timing_mark(TK_REDO, true, st);
-      e = launch_k(redo, (unsigned)num_sms() * 2, 128, smem, st, a);
-      if (e != cudaSuccess) return e;
-      if (t) timing_mark(TK_REDO, false, st);
       g_launches.fetch_add(1, std::memory_order_relaxed);
       return cudaGetLastError();
     }

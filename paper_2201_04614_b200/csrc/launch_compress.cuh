@@ -1,6 +1,6 @@
 // launch_compress.cuh -- per-shape launch of the compress kernels.
-//   fast shapes (3-D b=8/16, 2-D b=8/16) with 16-byte aligned rows:
-//       dq_compress_fast_kernel  +  int64 redo of listed tiles
+//   fast shapes (2-D / 3-D, b = 8 ... 64) with 16-byte aligned rows:
+//       dq_compress_fast_kernel (its warps redo int32-unsafe tiles in int64 themselves)
 //   everything else: dq_compress_kernel (generic, uint32/int64 per tile)
 #pragma once
 
@@ -70,32 +70,16 @@ cudaError_t run_compress_shape(const CompressArgs& a, cudaStream_t st) {
       if (grid > need) grid = need;
       if (grid < 1) grid = 1;
       fa.c = a;
-      fa.redo_count = const_cast<unsigned int*>(a.redo_count);
-      fa.redo_list = const_cast<long long*>(a.redo_list);
       const bool t = g_timing.load(std::memory_order_relaxed);
       if (t) timing_mark(TK_COMPRESS, true, st);
       e = launch_k(kern, (unsigned)grid, FAST_WARPS * 32, fsmem, st, fa);
       if (e != cudaSuccess) return e;
       if (t) timing_mark(TK_COMPRESS, false, st);
       g_launches.fetch_add(1, std::memory_order_relaxed);
-      e = cudaGetLastError();
-      if (e != cudaSuccess) return e;
-      // int64 redo of tiles whose |d| reached 2^24 (usually none: exits at once)
-      auto redo = dq_compress_kernel<ND, B, VPL, MODE, true>;
-      if (smem > 48 * 1024) {
-        int rps = 0;
-        e = occupancy(redo, 128, smem, rps);  // (its smem opt-in, once)
-        if (e != cudaSuccess) return e;
-      }
-      if (t) timing_mark(TK_REDO, true, st);
-      e = launch_k(redo, (unsigned)num_sms(), 128, smem, st, a);
-      if (e != cudaSuccess) return e;
-      if (t) timing_mark(TK_REDO, false, st);
-      g_launches.fetch_add(1, std::memory_order_relaxed);
       return cudaGetLastError();
     }
   }
-  return launch_tiles(dq_compress_kernel<ND, B, VPL, MODE, false>, a.g.ntiles, smem, st, a);
+  return launch_tiles(dq_compress_kernel<ND, B, VPL, MODE>, a.g.ntiles, smem, st, a);
 }
 
 template <int ND, int B, int VPL, int MODE>

@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <chrono>
 #include <cstdio>
 #include <tuple>
 #include <map>
@@ -73,13 +74,20 @@ cudaError_t occupancy_cached(const void* kern, int block, int smem, int& per_sm)
       return cudaSuccess;
     }
   }
-  if (smem > 48 * 1024) {
+  if (smem > 40 * 1024) {  // (with margin for a kernel's small static arrays)
     const cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
   }
   const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, block, smem);
   if (e != cudaSuccess) return e;
+  static const bool dbg = std::getenv("VLZ_DEBUG_OCC") != nullptr;
+  if (dbg) {
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, kern);
+    std::fprintf(stderr, "vlz_gpu: kernel %p block %d dyn smem %d static %zu regs %d local %zu -> %d CTAs/SM\n",
+                 kern, block, smem, fa.sharedSizeBytes, fa.numRegs, fa.localSizeBytes, per_sm);
+  }
   std::lock_guard<std::mutex> lk(mu);
   cache[key] = per_sm;
   return cudaSuccess;
@@ -105,7 +113,6 @@ int num_sms() {
 
 namespace {
 
-constexpr unsigned long long I64MAX = 0x7fffffffffffffffull;
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -157,15 +164,17 @@ bool valid_params(const vlz_params* p) {
   return true;
 }
 
+constexpr size_t REDO_SLACK = 65536;  // >= 8 * (warps of the largest persistent grid)
+
 // workspace layout
 struct WS {
   unsigned int* ticket;      // scan chunk ticket
   unsigned int* done;        // finished-CTA counter
-  unsigned int* redo_count;  // tiles queued for the int64 redo
+  unsigned long long* flag;  // per-call reset flag (InitArgs)
   long long* stats;          // sum, count, min, neg_max (single-GPU compress)
   long long* aux;            // 8 spare words
   unsigned long long* lb;    // look-back words, one per scan chunk
-  long long* redo_list;      // ntiles
+  long long* redo_list;      // ntiles + slack: per-warp slots of the int64 tails
   int64_t* offsets;          // nblocks
   float* scratch;            // N
   size_t bytes;
@@ -177,7 +186,7 @@ WS carve(const Geo& g, void* base) {
   size_t off = 0;
   w.ticket = reinterpret_cast<unsigned int*>(p + off);
   w.done = reinterpret_cast<unsigned int*>(p + off + 8);
-  w.redo_count = reinterpret_cast<unsigned int*>(p + off + 16);
+  w.flag = reinterpret_cast<unsigned long long*>(p + off + 32);
   w.stats = reinterpret_cast<long long*>(p + off + 64);
   w.aux = reinterpret_cast<long long*>(p + off + 128);
   off += 256;
@@ -185,7 +194,8 @@ WS carve(const Geo& g, void* base) {
   w.lb = reinterpret_cast<unsigned long long*>(p + off);
   off += align256((size_t)nchunks * 8);
   w.redo_list = reinterpret_cast<long long*>(p + off);
-  off += align256((size_t)g.ntiles * 8);
+  // slot k of warp w is entry k * nwarps + w: below ntiles + 8 * nwarps
+  off += align256(((size_t)g.ntiles + REDO_SLACK) * 8);
   w.offsets = reinterpret_cast<int64_t*>(p + off);
   off += align256((size_t)g.nblocks * 8);
   w.scratch = reinterpret_cast<float*>(p + off);
@@ -194,48 +204,32 @@ WS carve(const Geo& g, void* base) {
   return w;
 }
 
-// one tiny kernel resets the result block, the counters and look-back words
-__global__ void init_kernel(vlz_result* res, unsigned int* ticket, unsigned int* done,
-                            long long* stats, unsigned long long* lb, int64_t nchunks) {
-  pdl_enter();
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i == 0) {
-    if (res) {
-      res->status = 0;
-      res->reserved = 0;
-      res->index = -1;
-      res->n_outliers = 0;
-      res->first_nonfinite = (int64_t)I64MAX;
-      res->first_overflow = (int64_t)I64MAX;
-      res->first_bad_block = (int64_t)I64MAX;
-      res->sentinels = 0;
-      res->pad0 = 0;
-    }
-    *ticket = 0;
-    *done = 0;
-    ticket[4] = 0;  // redo_count (workspace offset 16)
-    if (stats) {
-      stats[0] = 0;
-      stats[1] = 0;
-      stats[2] = (long long)I64MAX;
-      stats[3] = (long long)I64MAX;
-    }
-  }
-  for (int64_t k = i; k < nchunks; k += (int64_t)gridDim.x * blockDim.x) lb[k] = 0;
+// Per-call reset record for the first kernel of a call (vlz_common.cuh
+// InitArgs): there is no init launch.  The nonce is unique per call in this
+// process and never 0 (the value the call's last kernel leaves in the flag, so
+// that a CUDA-graph replay of the same launches starts from a cleared flag).
+unsigned long long next_nonce() {
+  static std::atomic<unsigned long long> ctr{[] {
+    unsigned long long s =
+        (unsigned long long)std::chrono::steady_clock::now().time_since_epoch().count();
+    s ^= (unsigned long long)reinterpret_cast<uintptr_t>(&s) << 17;
+    return s * 0x9E3779B97F4A7C15ull;
+  }()};
+  unsigned long long v = ctr.fetch_add(1, std::memory_order_relaxed) + 1;
+  while (v == 0) v = ctr.fetch_add(1, std::memory_order_relaxed) + 1;
+  return v;
 }
 
-cudaError_t launch_init(vlz_result* res, const WS& w, long long* stats, int64_t nchunks,
-                        cudaStream_t st) {
-  int64_t blocks = (nchunks + 255) / 256;
-  if (blocks < 1) blocks = 1;
-  if (blocks > 1024) blocks = 1024;
-  const bool t = g_timing.load(std::memory_order_relaxed);
-  if (t) timing_mark(TK_INIT, true, st);
-  cudaError_t le = launch_k(init_kernel, (unsigned)blocks, 256, 0, st, res, w.ticket, w.done, stats, w.lb, nchunks);
-  if (le != cudaSuccess) return le;
-  if (t) timing_mark(TK_INIT, false, st);
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  return cudaGetLastError();
+InitArgs make_init(vlz_result* res, const WS& w, long long* stats, int64_t nchunks) {
+  InitArgs ia{};
+  ia.res = reinterpret_cast<unsigned long long*>(res);
+  ia.hdr = w.ticket;
+  ia.stats = stats;
+  ia.lb = w.lb;
+  ia.nchunks = nchunks;
+  ia.flag = w.flag;
+  ia.nonce = next_nonce();
+  return ia;
 }
 
 cudaError_t launch_scan(const ScanArgs& a, cudaStream_t st) {
@@ -388,9 +382,9 @@ __attribute__((visibility("hidden"))) int vlz_internal_compress_begin(const floa
   if (mode != MODE_ZERO && !d_scalars) return VLZ_E_ARG;
   if (mode == MODE_GLOBAL && !stats) return VLZ_E_ARG;
   const int64_t nchunks = scan_chunks(g.nblocks);
-  cudaError_t e = launch_init(d_result, w, stats, nchunks, st);
-  if (e != cudaSuccess) return to_rc(e);
+  cudaError_t e = cudaSuccess;
   CompressArgs a{};
+  a.init = make_init(d_result, w, stats, nchunks);
   a.g = g;
   a.q = make_qp(p);
   a.in = d_in;
@@ -405,7 +399,6 @@ __attribute__((visibility("hidden"))) int vlz_internal_compress_begin(const floa
   a.gcount = reinterpret_cast<unsigned long long*>(stats ? stats + 1 : nullptr);
   a.gmin = stats ? stats + 2 : nullptr;
   a.gnegmax = stats ? stats + 3 : nullptr;
-  a.redo_count = w.redo_count;
   a.redo_list = w.redo_list;
   const int b = gg->block_edge;
   if (gg->nd == 1) e = launch_compress_nd1(b, mode, a, st);
@@ -458,6 +451,7 @@ static int finish_impl(const float* d_in, const vlz_geom* gg, const vlz_params* 
   s.scalars = d_scalars;
   s.lb = w.lb;
   s.ticket = w.ticket;
+  s.flag = w.flag;
   s.n_out = reinterpret_cast<long long*>(&d_result->n_outliers);
   s.gstats = gstats;
   s.nstats = nstats;
@@ -542,10 +536,10 @@ static int decompress_impl(const void* d_codes, bool u32, const float* d_outlier
   const int mode = mode_of(p->pad_kind, p->pad_gran);
   if (mode != MODE_ZERO && !d_scalars) return VLZ_E_ARG;
   const int64_t nchunks = offsets_chunks(g.nblocks);
-  cudaError_t e = launch_init(d_result, w, nullptr, nchunks, st);
-  if (e != cudaSuccess) return to_rc(e);
+  cudaError_t e = cudaSuccess;
   const int b = gg->block_edge;
   ScanArgs s{};
+  s.init = make_init(d_result, w, nullptr, nchunks);
   s.g = g;
   s.q = make_qp(p);
   s.BZ = gg->nd == 3 ? b : 1;
@@ -579,8 +573,8 @@ static int decompress_impl(const void* d_codes, bool u32, const float* d_outlier
   a.status = &d_result->status;
   a.index = reinterpret_cast<long long*>(&d_result->index);
   a.n_sent_out = reinterpret_cast<long long*>(&d_result->n_outliers);
-  a.redo_count = w.redo_count;
   a.redo_list = w.redo_list;
+  a.flag = w.flag;
   return to_rc(launch_decompress(gg->nd, b, u32, a, st));
 }
 

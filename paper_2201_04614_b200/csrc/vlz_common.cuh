@@ -30,6 +30,74 @@ __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
+// Per-call reset of the result block and the workspace header, folded into the
+// first kernel of a call (there is no separate init launch).  CTA 0 of that
+// kernel resets the state and then publishes the call's nonce (unique per call
+// in this process, never the value a stale or uninitialised workspace holds
+// except with probability 2^-64) in the workspace's flag word; any thread of the
+// same grid that is about to touch the shared state (error minima, global
+// statistics, look-back words) first waits for the flag.  The waits sit on
+// rare paths or at the end of a CTA's work, long after CTA 0 -- the first CTA
+// the hardware dispatches -- has published.  Later kernels of the call are
+// ordered by the kernel boundary and need no wait.
+struct InitArgs {
+  unsigned long long* res;    // vlz_result as 8 64-bit words (nullptr: none)
+  unsigned int* hdr;          // workspace header: ticket (+0), done (+8 B), spare (+16 B)
+  long long* stats;           // sum, count, min, neg_max (nullptr: none)
+  unsigned long long* lb;     // look-back words of the call's scan kernel
+  long long nchunks;
+  unsigned long long* flag;
+  unsigned long long nonce;
+};
+
+__device__ __forceinline__ void ws_reset_scalars(const InitArgs& ia) {
+  constexpr long long I64MAX = 0x7fffffffffffffffll;
+  if (ia.res) {
+    ia.res[0] = 0ull;                        // status, reserved
+    ia.res[1] = ~0ull;                       // index = -1
+    ia.res[2] = 0ull;                        // n_outliers
+    ia.res[3] = (unsigned long long)I64MAX;  // first_nonfinite
+    ia.res[4] = (unsigned long long)I64MAX;  // first_overflow
+    ia.res[5] = (unsigned long long)I64MAX;  // first_bad_block
+    ia.res[6] = 0ull;                        // sentinels
+    ia.res[7] = 0ull;
+  }
+  ia.hdr[0] = 0u;  // ticket
+  ia.hdr[2] = 0u;  // done
+  ia.hdr[4] = 0u;
+  if (ia.stats) {
+    ia.stats[0] = 0;
+    ia.stats[1] = 0;
+    ia.stats[2] = I64MAX;
+    ia.stats[3] = I64MAX;
+  }
+}
+__device__ __forceinline__ void ws_publish(const InitArgs& ia) {  // release: orders the reset before it
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(ia.flag), "l"(ia.nonce) : "memory");
+}
+// the reset by one warp (warp 0 of CTA 0 of the fused compress kernels, after
+// it has issued its first loads, so the stores overlap their latency)
+__device__ __forceinline__ void ws_reset_warp(const InitArgs& ia, int lane) {
+  for (long long k = lane; k < ia.nchunks; k += 32) ia.lb[k] = 0ull;
+  if (lane == 0) ws_reset_scalars(ia);
+  __syncwarp();
+  if (lane == 0) ws_publish(ia);
+}
+// ... by every thread of CTA 0 (the offsets kernel of a decompress call)
+__device__ __forceinline__ void ws_reset_cta0(const InitArgs& ia) {
+  for (long long k = threadIdx.x; k < ia.nchunks; k += blockDim.x) ia.lb[k] = 0ull;
+  if (threadIdx.x == 0) ws_reset_scalars(ia);
+  __syncthreads();
+  if (threadIdx.x == 0) ws_publish(ia);
+}
+
+__device__ __forceinline__ void ws_wait(const InitArgs& ia) {
+  unsigned long long v;
+  do {
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ia.flag) : "memory");
+  } while (v != ia.nonce);
+}
+
 // Division of 32-bit unsigned values by a launch-invariant divisor d >= 1
 // (Granlund-Montgomery with the add-shift fix-up; exact for every x < 2^32).
 struct FastDiv {
