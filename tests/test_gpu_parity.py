@@ -255,6 +255,29 @@ def test_int64_redo_path(oracle):
         _check_full(oracle, d, 0.9, 8, pol, 32768)
 
 
+@pytest.mark.parametrize("shape,b", [((24, 40, 256), 8), ((33, 50, 260), 8), ((32, 48, 256), 16),
+                                     ((64, 64, 128), 32), ((70, 130, 136), 64), ((128, 128, 64), 64),
+                                     ((96, 512), 8), ((100, 516), 16), ((128, 512), 32),
+                                     ((130, 260), 64)])
+def test_fused_kernels_int64_tails(oracle, shape, b):
+    # 16-byte aligned rows keep the fused 2-D / 3-D kernels eligible; a slab of
+    # values near 1e9 at eb 0.9 pushes |d| past 2^24 (compress) and 2^27
+    # (decompress) in SOME tiles, so the warps that meet them redo them in
+    # int64 after their loops (compress_redo_tail / decompress_redo_tail; the
+    # b >= 32 3-D shapes take turns on the CTA's shared memory) while the rest
+    # of the grid stays on the int32 path
+    rng = np.random.default_rng(sum(shape) * 7 + b)
+    idx = np.indices(shape).astype(np.float64)
+    data = sum(np.sin(0.06 * (k + 1) * idx[k]) * 300.0 for k in range(len(shape)))
+    data = (data + rng.normal(0, 2.0, shape)).astype(np.float32)
+    data[..., -5:] *= np.float32(3.0e6)  # a few wide columns in the last window
+    lo, n = shape[0] // 3, max(3, shape[0] // 4)
+    data[lo:lo + n] = (rng.uniform(-1, 1, data[lo:lo + n].shape) * 1.0e9).astype(np.float32)
+    for pol in ("mean:global", "zero", "max:block", "min:edge"):
+        s = _check_full(oracle, data, 0.9, b, pol, 32768)
+        assert s.outlier_values.size > 0
+
+
 @pytest.mark.parametrize("shape,b", [((21, 44, 260), 8), ((19, 44, 196), 16),
                                      ((45, 300), 8), ((37, 196), 16), ((9, 12, 132), 8)])
 def test_fast_kernel_edge_tiles(oracle, shape, b):
@@ -437,3 +460,70 @@ def test_fused_kernels_error_precedence(shape, b):
     with pytest.raises(BoundTooSmallError) as err:
         dualquant_vector(d2.reshape(shape), _cfg(eb, b, "zero", 512))
     assert err.value.index == ovf_at
+
+
+def test_cuda_graph_replay_resets_per_call_state(oracle):
+    # the per-call reset lives in the first kernel of each call, guarded by a
+    # nonce baked into the launch: a captured graph replays the same nonce, so
+    # the call's last kernel must leave the flag cleared.  Replays over new
+    # input contents (global statistics, error minima, look-back words and the
+    # result block are all per-call state) must match the oracle every time.
+    import torch
+    from paper_2201_04614_b200 import gpu
+
+    shape, b, radius, pol = (40, 72, 256), 8, 512, "mean:global"
+    cfg = _cfg(1e-3, b, pol, radius)
+    rng = np.random.default_rng(5)
+    idx = np.indices(shape).astype(np.float64)
+
+    def field(k):
+        d = sum(np.sin(0.05 * (j + 1 + k) * idx[j]) * (3.0 + k) for j in range(3)) + 10.0 * k
+        return (d + rng.normal(0, 0.01, shape)).astype(np.float32)
+
+    x = torch.from_numpy(field(0)).cuda()
+    dev = gpu.compress_device(x, cfg, eb=1e-3).check()
+    y = torch.empty_like(x)
+    res = torch.empty(8, dtype=torch.int64, device="cuda")
+
+    import ctypes
+
+    from paper_2201_04614_b200 import _lib
+
+    lib = _lib.load()
+    g = _lib.geom(dev.grid.descriptor.dims, b)
+    p = _lib.params(1e-3, radius, cfg.padding.kind_code, cfg.padding.gran_code)
+    wsb = lib.vlz_workspace_size(ctypes.byref(g))
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")  # same workspace for both directions
+
+    def step():
+        st = torch.cuda.current_stream().cuda_stream
+        gpu.compress_device(x, cfg, eb=1e-3, out=dev, workspace=ws)
+        rc = lib.vlz_dq_decompress_dn(dev.codes.data_ptr(), dev.outliers.data_ptr(),
+                                      dev.result[2:3].data_ptr(), dev.counts.data_ptr(),
+                                      dev.scalars.data_ptr(), ctypes.byref(g), ctypes.byref(p),
+                                      y.data_ptr(), res.data_ptr(), ws.data_ptr(), wsb, st)
+        assert rc == 0
+
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        step()
+    torch.cuda.current_stream().wait_stream(side)
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr):
+        step()
+    for k in range(1, 5):
+        data = field(k)
+        x.copy_(torch.from_numpy(data))
+        gr.replay()
+        torch.cuda.synchronize()
+        o = oracle.dualquant(data, 1e-3, b, radius, pol)
+        assert np.array_equal(dev.codes.cpu().numpy().view(np.uint16).astype(np.uint32), o["codes"]), k
+        n = int(dev.result.cpu()[2])
+        assert n == o["outlier_values"].size
+        assert dev.outliers[:n].cpu().numpy().tobytes() == o["outlier_values"].tobytes()
+        assert np.array_equal(dev.scalars.cpu().numpy(), o["scalars"])
+        back = oracle.reconstruct(o["codes"], o["outlier_values"], o["outlier_counts"], o["scalars"],
+                                  shape, b, 1e-3, radius, pol)
+        assert y.cpu().numpy().tobytes() == back.tobytes(), k
+        assert int(res.cpu()[0]) == 0
