@@ -96,7 +96,11 @@ typedef struct vlz_stats {
 int64_t vlz_block_count(const vlz_geom* g);
 /* PaddingPolicy.scalar_count (model.py:167-175) */
 int64_t vlz_scalar_count(const vlz_geom* g, int32_t pad_kind, int32_t pad_gran);
-/* Device workspace bytes needed by compress/decompress for this geometry. */
+/* Device workspace bytes needed by compress/decompress for this geometry.
+ * The workspace needs no initialisation and may be reused across calls and
+ * geometries: the first kernel of every call resets the state the call uses
+ * (there is no separate init launch).  One workspace serves one call at a
+ * time (calls ordered on one stream, or otherwise not overlapping). */
 size_t vlz_workspace_size(const vlz_geom* g);
 
 /* ---- compress: replaces vector.dualquant_vector (vector.py:205-260) ---- *
@@ -262,8 +266,10 @@ int vlz_crc32_device(const uint8_t* d_data, int64_t n, uint32_t* d_crc, void* d_
 int64_t vlz_launch_count(void);
 /* per-kernel CUDA-event timing: when enabled every launch is bracketed by
  * events on its stream; collect() synchronises and returns, per kind
- * (0 init, 1 fused compress, 2 compress scan/gather, 3 decompress scan,
- * 4 fused decompress, 5 minmax), the summed milliseconds and launch counts
+ * (0 unused since the reset moved into the first kernel, 1 fused compress,
+ * 2 compress scan/gather, 3 decompress scan, 4 fused decompress, 5 minmax,
+ * 6 unused since the fused kernels redo int32-unsafe tiles themselves), the
+ * summed milliseconds and launch counts
  * since the last collect. */
 void vlz_timing(int enable);
 int vlz_timing_collect(double* ms, int64_t* launches, int n);
