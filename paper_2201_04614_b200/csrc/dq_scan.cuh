@@ -190,11 +190,20 @@ __device__ __forceinline__ T cta_excl_scan(T v, T* s_warp, T& total) {
 // per-block side array (read coalesced) and goes straight into the compact
 // array; the other outliers come from the block's scratch slots 1.. (0.. when
 // a non-global origin sits in slot 0).
+#ifndef VLZ_SCAN_HEAVY
+#define VLZ_SCAN_HEAVY 8
+#endif
+#ifndef VLZ_SCAN_HB
+#define VLZ_SCAN_HB 4
+#endif
+#ifndef VLZ_SCAN_MINB
+#define VLZ_SCAN_MINB 3
+#endif
 template <int SCAN_IPT>
-__global__ void __launch_bounds__(SCAN_THREADS) dq_scan_kernel(ScanArgs a) {
+__global__ void __launch_bounds__(SCAN_THREADS, VLZ_SCAN_MINB) dq_scan_kernel(ScanArgs a) {
   pdl_enter();
   constexpr int SCAN_CH = SCAN_THREADS * SCAN_IPT;
-  constexpr int HEAVY = 32;  // blocks with >= HEAVY scratch outliers: whole-warp copy
+  constexpr int HEAVY = VLZ_SCAN_HEAVY;  // blocks with >= HEAVY scratch outliers: whole-warp copy
   // padded so that both the coalesced ([k][tid]) and the per-thread
   // ([tid][k]) access patterns are (nearly) bank-conflict free
   __shared__ long long s_rec[SCAN_CH + SCAN_THREADS];  // count records in, final counts out
@@ -380,6 +389,39 @@ __global__ void __launch_bounds__(SCAN_THREADS) dq_scan_kernel(ScanArgs a) {
     for (int k = 0; k < SCAN_IPT; ++k)
       if (t < rem[k]) outc[dst[k] + t] = v[k];
   }
+  // heavy blocks (>= HEAVY outliers): whole-warp copies, HB blocks per batch
+  // so that their loads are in flight together (one block at a time left each
+  // block's ~0.7 us round trip exposed: 32 x SCAN_IPT of them per warp on an
+  // outlier-heavy field)
+  constexpr int HB = VLZ_SCAN_HB;
+  int bn[HB], bd[HB];
+  int64_t bs[HB];
+  int cnt = 0;
+  auto flush = [&]() {
+    int nmax = 0;
+#pragma unroll
+    for (int u = 0; u < HB; ++u) nmax = (u < cnt && bn[u] > nmax) ? bn[u] : nmax;
+    for (int t0 = 0; t0 < nmax; t0 += 128) {
+      float v[HB][4];
+#pragma unroll
+      for (int u = 0; u < HB; ++u) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int t = t0 + lane + 32 * j;
+          if (u < cnt && t < bn[u]) v[u][j] = __ldg(scratch + bs[u] + t);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < HB; ++u) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int t = t0 + lane + 32 * j;
+          if (u < cnt && t < bn[u]) outc[bd[u] + t] = v[u][j];
+        }
+      }
+    }
+    cnt = 0;
+  };
   unsigned hm = __ballot_sync(FULL, heavy != 0);
   while (hm) {
     const int src_lane = __ffs(hm) - 1;
@@ -391,22 +433,19 @@ __global__ void __launch_bounds__(SCAN_THREADS) dq_scan_kernel(ScanArgs a) {
       const int first = __shfl_sync(FULL, (int)((omask >> k) & 1u), src_lane);
       const int n = __shfl_sync(FULL, c[k], src_lane) - first;
       const int d0 = __shfl_sync(FULL, dst[k], src_lane);
-      const int64_t s = __shfl_sync(FULL, src[k], src_lane);
-      for (int t0 = 0; t0 < n; t0 += 128) {
-        float v[4];
+      const int64_t sb = __shfl_sync(FULL, src[k], src_lane);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int t = t0 + lane + 32 * j;
-          if (t < n) v[j] = __ldg(scratch + s + t);
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int t = t0 + lane + 32 * j;
-          if (t < n) outc[d0 + t] = v[j];
+      for (int u = 0; u < HB; ++u) {
+        if (cnt == u) {
+          bn[u] = n;
+          bd[u] = d0;
+          bs[u] = sb;
         }
       }
+      if (++cnt == HB) flush();
     }
   }
+  if (cnt) flush();
 }
 
 // Decompress: exclusive per-block outlier offsets (counts are the stream's
@@ -418,14 +457,18 @@ __global__ void __launch_bounds__(SCAN_THREADS) dq_scan_kernel(ScanArgs a) {
 // offsets, 2048 blocks per sweep staged through shared memory.
 constexpr int OFF_IPT = 8;
 constexpr int OFF_SWEEP = SCAN_THREADS * OFF_IPT;
-inline int64_t offsets_span(int64_t nblocks) {
-  // ~4 ranges per SM, at least one sweep each
-  int64_t span = (nblocks + 148 * 4 - 1) / (148 * 4);
+// `ranges` = the CTAs of this kernel the device holds at once (occupancy x
+// SMs, a few per SM): one range per resident CTA, at least one sweep each, so
+// that every CTA of the grid is resident and the blockIdx-ordered look-back
+// below never waits on a CTA that has not started
+inline int64_t offsets_span(int64_t nblocks, int64_t ranges) {
+  if (ranges < 1) ranges = 1;
+  int64_t span = (nblocks + ranges - 1) / ranges;
   span = (span + OFF_SWEEP - 1) / OFF_SWEEP * OFF_SWEEP;
   return span < OFF_SWEEP ? OFF_SWEEP : span;
 }
-inline int64_t offsets_chunks(int64_t nblocks) {
-  const int64_t span = offsets_span(nblocks);
+inline int64_t offsets_chunks(int64_t nblocks, int64_t ranges) {
+  const int64_t span = offsets_span(nblocks, ranges);
   const int64_t n = (nblocks + span - 1) / span;
   return n < 1 ? 1 : n;
 }
@@ -438,10 +481,10 @@ __global__ void __launch_bounds__(SCAN_THREADS) dq_offsets_kernel(ScanArgs a, in
   __shared__ long long s_wsum[SCAN_THREADS / 32];
   const int tid = threadIdx.x;
   // first kernel of a decompress call: CTA 0 resets the result block, the
-  // header and the look-back words (no init launch).  Ranges go by blockIdx
-  // (at most ~4 CTAs per SM exist, all resident or dispatched in index order,
-  // so every predecessor of a waiting CTA is running); the look-back words are
-  // first touched after the range sum, behind the reset flag.
+  // header and the look-back words (no init launch).  Ranges go by blockIdx:
+  // the grid is sized to the resident CTA count (offsets_span), so every
+  // predecessor of a waiting CTA is running; the look-back words are first
+  // touched after the range sum, behind the reset flag.
   if (blockIdx.x == 0) ws_reset_cta0(a.init);
   const int64_t tile = blockIdx.x;
   const int64_t nb = a.g.nblocks;

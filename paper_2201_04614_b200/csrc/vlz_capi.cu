@@ -232,6 +232,14 @@ InitArgs make_init(vlz_result* res, const WS& w, long long* stats, int64_t nchun
   return ia;
 }
 
+// resident CTAs of the offsets kernel on this device (its grid never exceeds it)
+int64_t offsets_ranges() {
+  int per_sm = 0;
+  if (occupancy(dq_offsets_kernel, SCAN_THREADS, 0, per_sm) != cudaSuccess || per_sm < 1) per_sm = 1;
+  if (per_sm > 4) per_sm = 4;
+  return (int64_t)per_sm * num_sms();
+}
+
 cudaError_t launch_scan(const ScanArgs& a, cudaStream_t st) {
   const bool t = g_timing.load(std::memory_order_relaxed);
   const int kind = a.gather ? TK_SCAN_C : TK_SCAN_D;
@@ -246,8 +254,10 @@ cudaError_t launch_scan(const ScanArgs& a, cudaStream_t st) {
       default: le = launch_k(dq_scan_kernel<8>, nchunks, SCAN_THREADS, 0, st, a); break;
     }
   } else {
-    const unsigned nchunks = (unsigned)offsets_chunks(a.g.nblocks);
-    le = launch_k(dq_offsets_kernel, nchunks, SCAN_THREADS, 0, st, a, offsets_span(a.g.nblocks));
+    const int64_t ranges = offsets_ranges();
+    const unsigned nchunks = (unsigned)offsets_chunks(a.g.nblocks, ranges);
+    le = launch_k(dq_offsets_kernel, nchunks, SCAN_THREADS, 0, st, a,
+                  offsets_span(a.g.nblocks, ranges));
   }
   if (t) timing_mark(kind, false, st);
   g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -535,7 +545,7 @@ static int decompress_impl(const void* d_codes, bool u32, const float* d_outlier
   if (ws_bytes < w.bytes) return VLZ_E_ARG;
   const int mode = mode_of(p->pad_kind, p->pad_gran);
   if (mode != MODE_ZERO && !d_scalars) return VLZ_E_ARG;
-  const int64_t nchunks = offsets_chunks(g.nblocks);
+  const int64_t nchunks = offsets_chunks(g.nblocks, offsets_ranges());
   cudaError_t e = cudaSuccess;
   const int b = gg->block_edge;
   ScanArgs s{};
