@@ -288,6 +288,16 @@ int vlz_test_prequant_sweep(double eb, unsigned long long* d_counts, void* strea
 /* 1 when the fast path is enabled for this eb (1/(2eb) in (2^-100, 2^100)) */
 int vlz_test_fast_enabled(double eb);
 
+/* ---- measurement support (not a product path; bench.py) -------------- *
+ * One arithmetic-free streaming kernel over n_elems elements (a multiple of
+ * 8, 16-byte aligned buffers) with the read : write mix of a fused kernel:
+ * kind 0 copy f32 -> f32 (4 B read + 4 B written per element), 1 narrow
+ * f32 -> u16 (4 + 2: the compress mix), 2 widen u16 -> f32 (2 + 4: the
+ * decompress mix); ctas_per_sm (1..8) CTAs of 256 threads per SM.  The caller
+ * times it with events on `stream`. */
+int vlz_bench_stream(int32_t kind, const void* d_src, void* d_dst, int64_t n_elems,
+                     int32_t ctas_per_sm, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -96,6 +96,7 @@ PROTOTYPES = {
     "vlz_version": (ctypes.c_char_p, []),
     "vlz_test_prequant_sweep": (ctypes.c_int, [ctypes.c_double, _vp, _vp]),
     "vlz_test_fast_enabled": (ctypes.c_int, [ctypes.c_double]),
+    "vlz_bench_stream": (ctypes.c_int, [ctypes.c_int32, _vp, _vp, _i64, ctypes.c_int32, _vp]),
 }
 
 _lib = None
