@@ -637,6 +637,10 @@ def run_ours(args):
             "decompress_gbs": in_bytes / (td / K * 1e-3) / 1e9,
             "kernel_ms_per_step": {"fused_compress": k1 / K, "fused_decompress": k4 / K,
                                    "compress_scan_gather": kms[2] / K, "decompress_scan": kms[3] / K},
+            "device_bytes": {"input": 4 * n, "codes": 2 * n, "outlier_array_worst_case": 4 * n,
+                             "outliers_in_stream": 4 * n_out, "counts": 8 * nb, "workspace": wsb,
+                             "decompressed": 4 * n,
+                             "note": "per rank; vlz_dq_compress_capped sizes the outlier array to the stream"},
             "launches_per_step": {"compress": 2, "decompress": 2,
                                   "note": "fused kernel (resets the per-call state itself) + scan; no init or redo launches"},
             "n_outliers": n_out_total,

@@ -42,6 +42,7 @@ extern "C" {
 #define VLZ_ST_EXHAUSTED 5       /* CorruptStreamError: outliers exhausted        */
 #define VLZ_ST_LEFTOVER 6        /* CorruptStreamError: leftover outliers         */
 #define VLZ_ST_SENTINEL_TOTAL 7  /* CorruptStreamError: sentinels != outliers     */
+#define VLZ_ST_OUTLIER_CAPACITY 8 /* vlz_dq_compress_capped: more outliers than the caller's array holds */
 
 /* padding policy codes: container.py:57-58 ordering */
 #define VLZ_PAD_ZERO 0
@@ -116,6 +117,19 @@ int vlz_dq_compress(const float* d_in, const vlz_geom* g, const vlz_params* p,
                     uint16_t* d_codes, float* d_outliers, int64_t* d_counts,
                     int64_t* d_scalars, vlz_result* d_result, void* d_ws,
                     size_t ws_bytes, void* stream);
+
+/* The same compression with an outlier array of `outlier_capacity` floats
+ * (any size from 0 to N; vlz_dq_compress needs the worst case, N).  Codes,
+ * counts, scalars and n_outliers are always complete.  When the stream has
+ * more outliers than fit, d_outliers holds the first outlier_capacity of them
+ * and the status is VLZ_ST_OUTLIER_CAPACITY: call again with at least
+ * n_outliers floats.  With the 8-slots-per-block scratch of the workspace this
+ * bounds the device memory of a compression by the stream it produces
+ * (C5: 17.2 GB in + 8.6 GB codes + 0.3 GB workspace + the outliers kept). */
+int vlz_dq_compress_capped(const float* d_in, const vlz_geom* g, const vlz_params* p,
+                           uint16_t* d_codes, float* d_outliers, int64_t outlier_capacity,
+                           int64_t* d_counts, int64_t* d_scalars, vlz_result* d_result,
+                           void* d_ws, size_t ws_bytes, void* stream);
 
 /* Two-phase form for slab-sharded multi-GPU runs (each rank compresses a
  * block-aligned slab along dims[0]).  begin = fused prequant + Lorenzo +

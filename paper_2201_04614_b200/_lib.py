@@ -38,6 +38,7 @@ assert ctypes.sizeof(Result) == 64
 # status codes (VLZ_ST_*)
 ST_OK, ST_NONFINITE, ST_OVERFLOW = 0, 1, 2
 ST_CORRUPT_CODE, ST_EXHAUSTED, ST_LEFTOVER, ST_SENTINEL_TOTAL = 4, 5, 6, 7
+ST_OUTLIER_CAPACITY = 8
 
 # exported symbols and their prototypes (must match include/vlz_gpu.h)
 _P = ctypes.POINTER
@@ -49,6 +50,8 @@ PROTOTYPES = {
     "vlz_workspace_size": (ctypes.c_size_t, [_P(Geom)]),
     "vlz_dq_compress": (ctypes.c_int, [_vp, _P(Geom), _P(Params), _vp, _vp, _vp, _vp, _vp, _vp,
                                        ctypes.c_size_t, _vp]),
+    "vlz_dq_compress_capped": (ctypes.c_int, [_vp, _P(Geom), _P(Params), _vp, _vp, _i64, _vp, _vp,
+                                              _vp, _vp, ctypes.c_size_t, _vp]),
     "vlz_dq_compress_begin": (ctypes.c_int, [_vp, _P(Geom), _P(Params), _vp, _vp, _vp, _vp, _vp,
                                              _vp, ctypes.c_size_t, _vp]),
     "vlz_dq_compress_finish": (ctypes.c_int, [_vp, _P(Geom), _P(Params), _vp, _vp, _vp, _vp, _vp,

@@ -280,11 +280,14 @@ __global__ void __launch_bounds__(D1_WARPS * 32, 4)
           cadd = 0u;
           const int excl = group_excl_scan<LPB>(__popc(om), lane, tot);
           const int64_t bstart = (e0 + (lane - gl) * VPL);  // block start = its first element
-          float* slot = a.scratch + bstart + 1 + excl;
-          int k = 0;
+          float* slot = a.scratch + (bstart / B) * SCRATCH_SLOTS + 1;
+          int k = excl;  // rank among the block's non-origin outliers
 #pragma unroll
           for (int j = 0; j < VPL; ++j)
-            if ((om >> j) & 1u) slot[k++] = v[j];
+            if ((om >> j) & 1u) {
+              if (k < SCRATCH_SLOTS - 1) slot[k] = v[j];
+              ++k;
+            }
         } else if (lead) {
           u[0] = 0u;  // packed below without a carry; the origin code is patched in
         }
@@ -308,7 +311,7 @@ __global__ void __launch_bounds__(D1_WARPS * 32, 4)
           int64_t total = tot;
           if (MODE != MODE_GLOBAL) {
             if (o_out) {
-              a.scratch[el] = v[0];
+              a.scratch[bi * SCRATCH_SLOTS] = v[0];
               total += 1;
             }
             if (MODE == MODE_BLOCK || MODE == MODE_EDGE) a.scalars[bi] = s0;

@@ -380,10 +380,13 @@ __device__ __forceinline__ void fast_tile(const FastArgs& fa, uint32_t tile, con
             int tot;
             const int excl = group_excl_scan<LPB>(__popc(om), lane, tot);
             int k = run + excl;
-            float* slot = a.scratch + bstart + 1;
+            float* slot = a.scratch + bi * SCRATCH_SLOTS + 1;
 #pragma unroll
             for (int j = 0; j < VPL; ++j)
-              if ((om >> j) & 1u) slot[k++] = vb[r][j];
+              if ((om >> j) & 1u) {
+                if (k < SCRATCH_SLOTS - 1) slot[k] = vb[r][j];
+                ++k;
+              }
             run += tot;
           }
         }
@@ -540,10 +543,13 @@ __device__ __forceinline__ void fast_tile(const FastArgs& fa, uint32_t tile, con
         int tot;
         const int excl = group_excl_scan<LPB>(__popc(om), lane, tot);
         int k = run + excl;
-        float* slot = a.scratch + bstart + 1;
+        float* slot = a.scratch + bi * SCRATCH_SLOTS + 1;
 #pragma unroll
         for (int j = 0; j < VPL; ++j)
-          if ((om >> j) & 1u) slot[k++] = v[j];
+          if ((om >> j) & 1u) {
+            if (k < SCRATCH_SLOTS - 1) slot[k] = v[j];
+            ++k;
+          }
         run += tot;
       }
       if (STAGE_CODES) {
@@ -682,7 +688,7 @@ __device__ __forceinline__ void fast_tile(const FastArgs& fa, uint32_t tile, con
       const bool o = bad_origin || d > (int64_t)(R - 1) || d < -(int64_t)(R - 1);
       a.codes[bstart] = o ? (uint16_t)0 : (uint16_t)(d + R);
       if (o) {
-        a.scratch[bstart] = v_origin;
+        a.scratch[bi * SCRATCH_SLOTS] = v_origin;
         total += 1;
       }
     }

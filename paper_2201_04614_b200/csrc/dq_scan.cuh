@@ -70,10 +70,17 @@ struct ScanArgs {
   // callers that copied the provisional codes out early (host pipeline)
   unsigned long long* patch_list;
   unsigned int* patch_count;
+  // floats the compact outlier array holds (vlz_dq_compress_capped); stores
+  // past it are dropped and the call ends with VLZ_ST_OUTLIER_CAPACITY
+  long long out_cap;
 };
 
-__device__ __forceinline__ void block_of(const Geo& g, int64_t bi, int BZ, int BY, int BX,
-                                         int64_t& bstart, int64_t& origin) {
+// element extents of a block along the padded dims
+struct BlockExt {
+  int ez, ey, ex;
+};
+__device__ __forceinline__ BlockExt block_of(const Geo& g, int64_t bi, int BZ, int BY, int BX,
+                                             int64_t& bstart, int64_t& origin) {
   int64_t bx, by, bz;
   if (g.nblocks < 0xffffffffll) {  // 32-bit magic division (the common case)
     const uint32_t t = g.divP2.div((uint32_t)bi);
@@ -90,6 +97,7 @@ __device__ __forceinline__ void block_of(const Geo& g, int64_t bi, int BZ, int B
   const int64_t ey = imin64(BY, g.D1 - by * BY);
   bstart = block_start(g, bz, by, bx, BZ, BY, BX, ez, ey);
   origin = ((bz * BZ) * g.D1 + by * BY) * g.D2 + bx * BX;
+  return BlockExt{(int)ez, (int)ey, (int)imin64(BX, g.D2 - bx * BX)};
 }
 
 constexpr unsigned long long FLAG_A = 1ull << 62;
@@ -178,6 +186,110 @@ __device__ __forceinline__ T cta_excl_scan(T v, T* s_warp, T& total) {
   return wbase + inc - v;
 }
 
+// The outliers of NB blocks from position p0 on, in canonical (code) order,
+// written to outp[u] by one warp: per block 512 codes per step (16 per lane,
+// loaded together), ranks by a byte-packed warp scan of the four 128-code
+// groups' zero counts, then the input values at the zero codes' coordinates.
+// The NB blocks go through each phase together, so their loads overlap (one
+// block at a time left ~3 dependent round trips per block exposed).
+template <int NB>
+__device__ __forceinline__ void regen_blocks(const ScanArgs& a, const int64_t (&bi)[NB], int nvalid,
+                                             int p0, float* const (&outp)[NB],
+                                             const int (&olim)[NB], int lane) {
+  int64_t origin[NB];
+  const uint16_t* cp[NB];
+  int nelem[NB], exy[NB], ex[NB], ey[NB], done[NB];
+  int nmax = 0;
+#pragma unroll
+  for (int u = 0; u < NB; ++u) {
+    int64_t bstart = 0;
+    origin[u] = 0;
+    BlockExt e{0, 0, 1};
+    if (u < nvalid) e = block_of(a.g, bi[u], a.BZ, a.BY, a.BX, bstart, origin[u]);
+    nelem[u] = e.ez * e.ey * e.ex;
+    ex[u] = e.ex;
+    ey[u] = e.ey > 0 ? e.ey : 1;
+    exy[u] = ex[u] * ey[u];
+    cp[u] = a.codes + bstart;
+    done[u] = 0;
+    nmax = nelem[u] > nmax ? nelem[u] : nmax;
+  }
+  const float* __restrict__ in = a.in;
+  for (int i0 = 0; i0 < nmax; i0 += 512) {
+    unsigned zm[NB], excl[NB], tot[NB];
+#pragma unroll
+    for (int u = 0; u < NB; ++u) {
+      zm[u] = 0;  // bit g*4+j: code (i0 + g*128 + lane*4 + j) is an outlier
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int i = i0 + g * 128 + lane * 4 + j;
+          const unsigned cv = (i >= p0 && i < nelem[u]) ? (unsigned)cp[u][i] : 1u;
+          zm[u] |= (cv == 0u) ? (1u << (g * 4 + j)) : 0u;
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < NB; ++u) {
+      // per-group counts packed in bytes (<= 128 each over the warp)
+      unsigned cnt = 0;
+#pragma unroll
+      for (int g = 0; g < 4; ++g) cnt |= (unsigned)__popc((zm[u] >> (g * 4)) & 15u) << (8 * g);
+      unsigned inc = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned v = __shfl_up_sync(FULL, inc, o);
+        if (lane >= o) inc += v;
+      }
+      tot[u] = __shfl_sync(FULL, inc, 31);
+      excl[u] = inc - cnt;
+    }
+    // all of the step's input loads first (independent), then the stores.
+    // A lane's 4 codes of a group are consecutive: their coordinates advance
+    // from the first one's (one division pair per group, not per element)
+    float val[NB][16];
+#pragma unroll
+    for (int u = 0; u < NB; ++u) {
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        const int ig = i0 + g * 128 + lane * 4;
+        const int z0 = ig / exy[u], r0 = ig - z0 * exy[u], y0 = r0 / ex[u];
+        int z = z0, y = y0, x = r0 - y0 * ex[u];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          val[u][g * 4 + j] = 0.f;
+          if ((zm[u] >> (g * 4 + j)) & 1u)
+            val[u][g * 4 + j] = __ldg(in + origin[u] + ((int64_t)z * a.g.D1 + y) * a.g.D2 + x);
+          if (++x == ex[u]) {
+            x = 0;
+            if (++y == ey[u]) {
+              y = 0;
+              ++z;
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < NB; ++u) {
+      int gbase = done[u];
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        int r = gbase + (int)((excl[u] >> (8 * g)) & 255u);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if ((zm[u] >> (g * 4 + j)) & 1u) {
+            if (r < olim[u]) outp[u][r] = val[u][g * 4 + j];
+            ++r;
+          }
+        gbase += (int)((tot[u] >> (8 * g)) & 255u);
+      }
+      done[u] = gbase;
+    }
+  }
+}
+
 // Compress: origin fix-up (*:global), count scan and outlier gather.  Thread t
 // owns blocks t*IPT .. t*IPT+IPT-1 of its chunk.  Order of work:
 //  1. counts from the records (shared memory) -> chunk scan -> the aggregate
@@ -194,7 +306,8 @@ __device__ __forceinline__ T cta_excl_scan(T v, T* s_warp, T& total) {
 #define VLZ_SCAN_HEAVY 8
 #endif
 #ifndef VLZ_SCAN_HB
-#define VLZ_SCAN_HB 4
+#define VLZ_SCAN_HB 1  // heavy blocks regenerated together by a warp (2: 193 us, 4: 358 us on the
+                       // outlier-stress field against 155 us -- the register arrays spill)
 #endif
 #ifndef VLZ_SCAN_MINB
 #define VLZ_SCAN_MINB 3
@@ -311,10 +424,10 @@ __global__ void __launch_bounds__(SCAN_THREADS, VLZ_SCAN_MINB) dq_scan_kernel(Sc
       rem[k] = c[k] - (int)((omask >> k) & 1u);
       src[k] = 0;
       if (((wmask >> k) & 1u) || rem[k] > 0) {
-        int64_t bstart, origin;
-        block_of(a.g, bi, a.BZ, a.BY, a.BX, bstart, origin);
-        src[k] = bstart + 1;
+        src[k] = bi * SCRATCH_SLOTS + 1;
         if ((wmask >> k) & 1u) {
+          int64_t bstart, origin;
+          block_of(a.g, bi, a.BZ, a.BY, a.BX, bstart, origin);
           a.codes[bstart] = ocode[k];
           if (a.patch_list)
             a.patch_list[atomicAdd(a.patch_count, 1u)] =
@@ -333,7 +446,7 @@ __global__ void __launch_bounds__(SCAN_THREADS, VLZ_SCAN_MINB) dq_scan_kernel(Sc
       if (c[k] > 0) {
         int64_t bstart, origin;
         block_of(a.g, bi, a.BZ, a.BY, a.BX, bstart, origin);
-        src[k] = bstart;
+        src[k] = bi * SCRATCH_SLOTS;
         code0[k] = a.codes[bstart];  // 0: the origin is an outlier in slot 0
       }
     }
@@ -366,18 +479,24 @@ __global__ void __launch_bounds__(SCAN_THREADS, VLZ_SCAN_MINB) dq_scan_kernel(Sc
       } else if (ov != 0x7fffffffffffffffull) {
         *a.status = 2;  // VLZ_ST_OVERFLOW
         *a.index = (long long)ov;
+      } else if (cexcl + agg > a.out_cap) {
+        *a.status = 8;  // VLZ_ST_OUTLIER_CAPACITY (n_outliers holds the true count)
+        *a.index = -1;
       }
     }
   }
   float* const outc = a.out + cexcl;
+  // chunk-relative positions below `lim` fit the caller's outlier array
+  const long long lim64 = a.out_cap - cexcl;
+  const int lim = lim64 > 0x7fffffffll ? 0x7fffffff : (lim64 < 0 ? 0 : (int)lim64);
   int dst[SCAN_IPT];
   int run = texcl;
 #pragma unroll
   for (int k = 0; k < SCAN_IPT; ++k) {
     const int first = (omask >> k) & 1u;
-    if (first) outc[run] = vo[k];
+    if (first && run < lim) outc[run] = vo[k];
     dst[k] = run + first;
-    if (rem[k] > 0) outc[dst[k]] = v0[k];
+    if (rem[k] > 0 && dst[k] < lim) outc[dst[k]] = v0[k];
     run += c[k];
   }
   for (int t = 1; t < tmax; ++t) {
@@ -387,41 +506,16 @@ __global__ void __launch_bounds__(SCAN_THREADS, VLZ_SCAN_MINB) dq_scan_kernel(Sc
       if (t < rem[k]) v[k] = __ldg(scratch + src[k] + t);
 #pragma unroll
     for (int k = 0; k < SCAN_IPT; ++k)
-      if (t < rem[k]) outc[dst[k] + t] = v[k];
+      if (t < rem[k] && dst[k] + t < lim) outc[dst[k] + t] = v[k];
   }
-  // heavy blocks (>= HEAVY outliers): whole-warp copies, HB blocks per batch
-  // so that their loads are in flight together (one block at a time left each
-  // block's ~0.7 us round trip exposed: 32 x SCAN_IPT of them per warp on an
-  // outlier-heavy field)
-  constexpr int HB = VLZ_SCAN_HB;
-  int bn[HB], bd[HB];
-  int64_t bs[HB];
+  // heavy blocks (>= HEAVY outliers, more than the block's scratch slots hold):
+  // a whole warp regenerates the values from the codes (0 marks an outlier)
+  // and the input, in canonical order
+  constexpr int NB = VLZ_SCAN_HB;
+  int64_t hb[NB];
+  float* ho[NB];
+  int hl[NB];
   int cnt = 0;
-  auto flush = [&]() {
-    int nmax = 0;
-#pragma unroll
-    for (int u = 0; u < HB; ++u) nmax = (u < cnt && bn[u] > nmax) ? bn[u] : nmax;
-    for (int t0 = 0; t0 < nmax; t0 += 128) {
-      float v[HB][4];
-#pragma unroll
-      for (int u = 0; u < HB; ++u) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int t = t0 + lane + 32 * j;
-          if (u < cnt && t < bn[u]) v[u][j] = __ldg(scratch + bs[u] + t);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < HB; ++u) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int t = t0 + lane + 32 * j;
-          if (u < cnt && t < bn[u]) outc[bd[u] + t] = v[u][j];
-        }
-      }
-    }
-    cnt = 0;
-  };
   unsigned hm = __ballot_sync(FULL, heavy != 0);
   while (hm) {
     const int src_lane = __ffs(hm) - 1;
@@ -430,22 +524,24 @@ __global__ void __launch_bounds__(SCAN_THREADS, VLZ_SCAN_MINB) dq_scan_kernel(Sc
 #pragma unroll
     for (int k = 0; k < SCAN_IPT; ++k) {
       if (!((mk >> k) & 1u)) continue;  // warp-uniform
-      const int first = __shfl_sync(FULL, (int)((omask >> k) & 1u), src_lane);
-      const int n = __shfl_sync(FULL, c[k], src_lane) - first;
       const int d0 = __shfl_sync(FULL, dst[k], src_lane);
-      const int64_t sb = __shfl_sync(FULL, src[k], src_lane);
+      const int64_t bi = base + (int64_t)(tid - lane + src_lane) * SCAN_IPT + k;
 #pragma unroll
-      for (int u = 0; u < HB; ++u) {
+      for (int u = 0; u < NB; ++u) {
         if (cnt == u) {
-          bn[u] = n;
-          bd[u] = d0;
-          bs[u] = sb;
+          hb[u] = bi;
+          ho[u] = outc + d0;
+          hl[u] = lim - d0;
         }
       }
-      if (++cnt == HB) flush();
+      // under *:global the origin (position 0) is settled above, from its record
+      if (++cnt == NB) {
+        regen_blocks<NB>(a, hb, NB, fix ? 1 : 0, ho, hl, lane);
+        cnt = 0;
+      }
     }
   }
-  if (cnt) flush();
+  if (cnt) regen_blocks<NB>(a, hb, cnt, fix ? 1 : 0, ho, hl, lane);
 }
 
 // Decompress: exclusive per-block outlier offsets (counts are the stream's

@@ -176,7 +176,7 @@ struct WS {
   unsigned long long* lb;    // look-back words, one per scan chunk
   long long* redo_list;      // ntiles + slack: per-warp slots of the int64 tails
   int64_t* offsets;          // nblocks
-  float* scratch;            // N
+  float* scratch;            // SCRATCH_SLOTS per block
   size_t bytes;
 };
 
@@ -199,7 +199,7 @@ WS carve(const Geo& g, void* base) {
   w.offsets = reinterpret_cast<int64_t*>(p + off);
   off += align256((size_t)g.nblocks * 8);
   w.scratch = reinterpret_cast<float*>(p + off);
-  off += align256((size_t)g.N * 4);
+  off += align256((size_t)g.nblocks * SCRATCH_SLOTS * 4);
   w.bytes = off;
   return w;
 }
@@ -421,7 +421,8 @@ static int finish_impl(const float* d_in, const vlz_geom* gg, const vlz_params* 
                        const long long* gstats, int nstats, uint16_t* d_codes,
                        float* d_outliers, int64_t* d_counts, int64_t* d_scalars,
                        vlz_result* d_result, void* d_ws, size_t ws_bytes, cudaStream_t st,
-                       unsigned long long* patch_list, unsigned int* patch_count);
+                       unsigned long long* patch_list, unsigned int* patch_count,
+                       long long out_cap = 0x7fffffffffffffffll);
 
 __attribute__((visibility("hidden"))) int vlz_internal_compress_finish(const float* d_in, const vlz_geom* gg, const vlz_params* p,
                                 const long long* gstats, uint16_t* d_codes, float* d_outliers,
@@ -436,7 +437,8 @@ static int finish_impl(const float* d_in, const vlz_geom* gg, const vlz_params* 
                        const long long* gstats, int nstats, uint16_t* d_codes,
                        float* d_outliers, int64_t* d_counts, int64_t* d_scalars,
                        vlz_result* d_result, void* d_ws, size_t ws_bytes, cudaStream_t st,
-                       unsigned long long* patch_list, unsigned int* patch_count) {
+                       unsigned long long* patch_list, unsigned int* patch_count,
+                       long long out_cap) {
   Geo g;
   if (!make_geo(gg, g, true) || !valid_params(p) || !d_outliers || !d_result || !d_ws)
     return VLZ_E_ARG;
@@ -472,6 +474,7 @@ static int finish_impl(const float* d_in, const vlz_geom* gg, const vlz_params* 
   s.first_overflow = reinterpret_cast<const unsigned long long*>(&d_result->first_overflow);
   s.patch_list = patch_list;
   s.patch_count = patch_count;
+  s.out_cap = out_cap;
   if (mode == MODE_GLOBAL && !gstats) return VLZ_E_ARG;
   return to_rc(launch_scan(s, st));
 }
@@ -488,6 +491,24 @@ int vlz_dq_compress(const float* d_in, const vlz_geom* g, const vlz_params* p, u
   if (rc != VLZ_OK) return rc;
   return vlz_internal_compress_finish(d_in, g, p, w.stats, d_codes, d_outliers, d_counts, d_scalars,
                               d_result, d_ws, ws_bytes, st, nullptr, nullptr);
+}
+
+int vlz_dq_compress_capped(const float* d_in, const vlz_geom* g, const vlz_params* p,
+                           uint16_t* d_codes, float* d_outliers, int64_t outlier_capacity,
+                           int64_t* d_counts, int64_t* d_scalars, vlz_result* d_result, void* d_ws,
+                           size_t ws_bytes, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Geo gg;
+  if (!make_geo(g, gg, true) || outlier_capacity < 0 || (outlier_capacity > 0 && !d_outliers))
+    return VLZ_E_ARG;
+  WS w = carve(gg, d_ws);
+  int rc = vlz_internal_compress_begin(d_in, g, p, d_codes, d_counts, d_scalars, d_result, w.stats,
+                                       d_ws, ws_bytes, st);
+  if (rc != VLZ_OK) return rc;
+  // (a zero-capacity call still needs a non-null pointer for the kernel's base address)
+  float* out = d_outliers ? d_outliers : reinterpret_cast<float*>(w.scratch);
+  return finish_impl(d_in, g, p, w.stats, 1, d_codes, out, d_counts, d_scalars, d_result, d_ws,
+                     ws_bytes, st, nullptr, nullptr, (long long)outlier_capacity);
 }
 
 int vlz_dq_compress_begin(const float* d_in, const vlz_geom* g, const vlz_params* p,

@@ -98,6 +98,12 @@ __device__ __forceinline__ void ws_wait(const InitArgs& ia) {
   } while (v != ia.nonce);
 }
 
+// Outlier scratch of the compress path: SCRATCH_SLOTS floats per block (slot 0
+// the block origin, 1.. its other outliers in traversal order).  A block with
+// more outliers than fit keeps only its count; the scan kernel regenerates its
+// values from the codes (code 0 marks them) and the input (dq_scan.cuh).
+constexpr int SCRATCH_SLOTS = 8;
+
 // Division of 32-bit unsigned values by a launch-invariant divisor d >= 1
 // (Granlund-Montgomery with the add-shift fix-up; exact for every x < 2^32).
 struct FastDiv {

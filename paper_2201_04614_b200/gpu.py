@@ -20,7 +20,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .errors import BoundTooSmallError, ConfigError, CorruptStreamError
+from .errors import BoundTooSmallError, ConfigError, CorruptStreamError, OutlierCapacityError
 from .model import (
     ArrayDescriptor,
     BlockGrid,
@@ -133,6 +133,8 @@ class DeviceCodeStream:
         if r.status == _lib.ST_OVERFLOW:
             v = float(self.source.reshape(-1)[r.index].item()) if self.source is not None else float("nan")
             raise BoundTooSmallError(int(r.index), v, self.eb)
+        if r.status == _lib.ST_OUTLIER_CAPACITY:
+            raise OutlierCapacityError(int(r.n_outliers), int(self.outliers.numel()))
         if r.status != _lib.ST_OK:
             raise RuntimeError(f"unexpected compress status {r.status}")
         return self
@@ -162,9 +164,13 @@ class Workspace:
 
 def compress_device(x: torch.Tensor, config: CompressionConfig, eb: float = None,
                     stream=None, workspace: torch.Tensor = None,
-                    out: DeviceCodeStream = None) -> DeviceCodeStream:
+                    out: DeviceCodeStream = None,
+                    outlier_capacity: int = None) -> DeviceCodeStream:
     """Fused dual-quant compress of a CUDA float32 tensor (no host sync unless
-    the bound is value-range relative)."""
+    the bound is value-range relative).  `outlier_capacity` bounds the outlier
+    array (default: the worst case, one slot per element); a stream with more
+    outliers makes check() raise OutlierCapacityError carrying the count to
+    retry with."""
     if not x.is_cuda:
         raise ConfigError("compress_device needs a CUDA tensor")
     desc = ArrayDescriptor.from_array(x)
@@ -185,7 +191,8 @@ def compress_device(x: torch.Tensor, config: CompressionConfig, eb: float = None
     if out is None:
         out = DeviceCodeStream(
             codes=_alloc_like(n, torch.int16, dev),
-            outliers=_alloc_like(n, torch.float32, dev),
+            outliers=_alloc_like(n if outlier_capacity is None else min(n, int(outlier_capacity)),
+                                 torch.float32, dev),
             counts=_alloc_like(grid.block_count, torch.int64, dev),
             scalars=torch.empty(ns, dtype=torch.int64, device=dev),
             result=torch.empty(8, dtype=torch.int64, device=dev),
@@ -196,11 +203,24 @@ def compress_device(x: torch.Tensor, config: CompressionConfig, eb: float = None
         out._host_result = None
     wsb = lib.vlz_workspace_size(ctypes.byref(g))
     ws = workspace if workspace is not None else Workspace.get(wsb, dev)
-    rc = lib.vlz_dq_compress(
-        _ptr(x), ctypes.byref(g), ctypes.byref(p), _ptr(out.codes), _ptr(out.outliers),
-        _ptr(out.counts), _ptr(out.scalars) if ns else None, _ptr(out.result), _ptr(ws),
-        ws.numel(), _stream(stream),
-    )
+    if outlier_capacity is not None and int(outlier_capacity) < 0:
+        raise ConfigError("outlier_capacity must be >= 0")
+    cap = min(n, int(out.outliers.numel())) if (outlier_capacity is not None or
+                                                out.outliers.numel() < n) else None
+    if cap is None:
+        rc = lib.vlz_dq_compress(
+            _ptr(x), ctypes.byref(g), ctypes.byref(p), _ptr(out.codes), _ptr(out.outliers),
+            _ptr(out.counts), _ptr(out.scalars) if ns else None, _ptr(out.result), _ptr(ws),
+            ws.numel(), _stream(stream),
+        )
+    else:
+        if outlier_capacity is not None:
+            cap = min(cap, int(outlier_capacity))
+        rc = lib.vlz_dq_compress_capped(
+            _ptr(x), ctypes.byref(g), ctypes.byref(p), _ptr(out.codes), _ptr(out.outliers), cap,
+            _ptr(out.counts), _ptr(out.scalars) if ns else None, _ptr(out.result), _ptr(ws),
+            ws.numel(), _stream(stream),
+        )
     if rc != 0:
         raise RuntimeError(f"vlz_dq_compress failed ({rc})")
     return out

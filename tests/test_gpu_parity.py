@@ -462,6 +462,84 @@ def test_fused_kernels_error_precedence(shape, b):
     assert err.value.index == ovf_at
 
 
+@pytest.mark.parametrize("shape,b", [((5000,), 8), ((70001,), 64), ((1 << 20,), 256),
+                                     ((4_500_000,), 256), ((45, 300), 8), ((37, 196), 16),
+                                     ((100, 516), 32), ((130, 260), 64), ((21, 44, 260), 8),
+                                     ((19, 44, 196), 16), ((40, 70, 136), 32), ((70, 130, 136), 64)])
+def test_dense_blocks_regenerated_from_codes(oracle, shape, b):
+    # the outlier scratch holds 8 slots per block; blocks with more outliers
+    # keep only their count and the scan kernel regenerates the values from the
+    # codes and the input (regen_block).  Noise far above radius * 2eb makes
+    # most elements outliers -- full and partial blocks, outlier and in-range
+    # origins, every policy family, fused and generic kernels, 1-D to 3-D.
+    prev = M.valid_block_edges()
+    M.allow_block_256(True)
+    try:
+        rng = np.random.default_rng(sum(shape) + 31 * b)
+        idx = np.indices(shape).astype(np.float64)
+        data = sum(np.sin(0.05 * (k + 1) * idx[k]) * 3.0 for k in range(len(shape)))
+        noise = rng.normal(0, 1.0, shape)
+        quiet = rng.random(shape) < 0.35  # some elements stay predictable
+        data = (data + np.where(quiet, 0.0, noise)).astype(np.float32)
+        for eb, pol, radius in ((1e-3, "zero", 16), (1e-3, "mean:global", 16),
+                                (2e-3, "max:block", 8), (1e-3, "min:edge", 32)):
+            s = _check_full(oracle, data, eb, b, pol, radius)
+            assert s.outlier_values.size > 0.3 * data.size
+            assert int(s.outlier_counts.max()) >= min(8, b - 1)
+    finally:
+        M.allow_block_256(256 in prev)
+
+
+@pytest.mark.parametrize("shape,b,pol", [((40, 72, 256), 8, "mean:global"), ((300, 516), 16, "zero"),
+                                         ((1 << 20,), 64, "max:block")])
+def test_capped_outlier_array(oracle, shape, b, pol):
+    # vlz_dq_compress_capped: an outlier array sized to the stream (not to the
+    # worst case).  Enough capacity: the same stream as the oracle's.  Too
+    # little: codes / counts / scalars complete, the first `capacity` outliers
+    # written, nothing past the array touched, status -> OutlierCapacityError
+    # carrying the true count; a retry with that count succeeds.
+    import torch
+    from paper_2201_04614_b200.errors import OutlierCapacityError
+
+    rng = np.random.default_rng(sum(shape) + b)
+    idx = np.indices(shape).astype(np.float64)
+    data = sum(np.sin(0.05 * (k + 1) * idx[k]) * 20.0 for k in range(len(shape)))
+    data = (data + rng.normal(0, 0.02, shape)).astype(np.float32)
+    data.ravel()[rng.integers(0, data.size, 4000)] *= 5.0  # spikes -> outliers, some blocks dense
+    eb, radius = 1e-3, 64
+    cfg = _cfg(eb, b, pol, radius)
+    o = oracle.dualquant(data, eb, b, radius, pol)
+    n_true = int(o["outlier_values"].size)
+    assert n_true > 100
+    x = torch.from_numpy(data).cuda()
+    # exact fit
+    dev = gpu.compress_device(x, cfg, eb=eb, outlier_capacity=n_true).check()
+    assert dev.outliers.numel() == n_true and dev.n_outliers == n_true
+    assert dev.outliers.cpu().numpy().tobytes() == o["outlier_values"].tobytes()
+    assert np.array_equal(dev.codes.cpu().numpy().view(np.uint16).astype(np.uint32), o["codes"])
+    # too small: guard words behind the array stay intact
+    cap = n_true // 3
+    small = gpu.compress_device(x, cfg, eb=eb, outlier_capacity=cap)
+    guard = torch.full((cap + 64,), float("nan"), dtype=torch.float32, device="cuda")
+    small.outliers = guard[:cap]
+    small = gpu.compress_device(x, cfg, eb=eb, out=small, outlier_capacity=cap)
+    with pytest.raises(OutlierCapacityError) as ei:
+        small.check()
+    assert ei.value.needed == n_true and ei.value.capacity == cap
+    assert bool(torch.isnan(guard[cap:]).all())
+    assert small.outliers.cpu().numpy().tobytes() == o["outlier_values"][:cap].tobytes()
+    assert np.array_equal(small.codes.cpu().numpy().view(np.uint16).astype(np.uint32), o["codes"])
+    assert np.array_equal(small.counts.cpu().numpy(), o["outlier_counts"])
+    assert np.array_equal(small.scalars.cpu().numpy(), o["scalars"])
+    # retry with the reported count
+    again = gpu.compress_device(x, cfg, eb=eb, outlier_capacity=ei.value.needed).check()
+    assert again.outliers.cpu().numpy().tobytes() == o["outlier_values"].tobytes()
+    # zero capacity is legal
+    none = gpu.compress_device(x, cfg, eb=eb, outlier_capacity=0)
+    with pytest.raises(OutlierCapacityError):
+        none.check()
+
+
 def test_cuda_graph_replay_resets_per_call_state(oracle):
     # the per-call reset lives in the first kernel of each call, guarded by a
     # nonce baked into the launch: a captured graph replays the same nonce, so
