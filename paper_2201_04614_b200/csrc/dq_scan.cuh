@@ -290,6 +290,83 @@ __device__ __forceinline__ void regen_blocks(const ScanArgs& a, const int64_t (&
   }
 }
 
+// The same regeneration by ONE thread for its own block: when most lanes of a
+// warp own dense blocks (an outlier-heavy field), 32 blocks advance together,
+// each lane walking its block 32 codes at a time, instead of one block per
+// warp pass (32 passes of ~3 dependent round trips each).
+__device__ __forceinline__ void regen_lane(const ScanArgs& a, int64_t bi, int p0, float* outp,
+                                           int olim) {
+  int64_t bstart, origin;
+  const BlockExt e = block_of(a.g, bi, a.BZ, a.BY, a.BX, bstart, origin);
+  const int nelem = e.ez * e.ey * e.ex;
+  const uint16_t* __restrict__ cp = a.codes + bstart;
+  const float* __restrict__ in = a.in;
+  const bool al = ((bstart & 7) == 0) && ((reinterpret_cast<uintptr_t>(a.codes) & 15) == 0);  // 16-byte aligned code vectors
+  int r = 0, x = 0, y = 0, z = 0;       // rank; coordinates of position i0
+  for (int i0 = 0; i0 < nelem; i0 += 32) {
+    unsigned zm = 0;  // bit j: code i0 + j is an outlier
+    if (al && i0 + 32 <= nelem) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint4 w = *reinterpret_cast<const uint4*>(cp + i0 + 8 * q);
+        const unsigned ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          zm |= ((ws[t] & 0xffffu) == 0u) ? (1u << (8 * q + 2 * t)) : 0u;
+          zm |= ((ws[t] >> 16) == 0u) ? (1u << (8 * q + 2 * t + 1)) : 0u;
+        }
+      }
+    } else {
+#pragma unroll 8
+      for (int j = 0; j < 32; ++j)
+        if (i0 + j < nelem && cp[i0 + j] == 0) zm |= 1u << j;
+    }
+    if (i0 == 0 && p0) zm &= ~1u;  // the origin is settled from its record
+    // the step's input loads together (8 at a time), then their stores
+    unsigned m = zm;
+    int cur = 0;  // codes of this step the coordinates have advanced over
+    while (m) {
+      float val[8];
+      int n = 0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        val[u] = 0.f;
+        if (m) {
+          const int j = __ffs(m) - 1;
+          m &= m - 1;
+          // advance (x, y, z) by j - cur positions
+          x += j - cur;
+          cur = j;
+          while (x >= e.ex) {
+            x -= e.ex;
+            if (++y == e.ey) {
+              y = 0;
+              ++z;
+            }
+          }
+          val[u] = __ldg(in + origin + ((int64_t)z * a.g.D1 + y) * a.g.D2 + x);
+          n = u + 1;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (u < n) {
+          if (r < olim) outp[r] = val[u];
+          ++r;
+        }
+    }
+    // to the first position of the next step
+    x += 32 - cur;
+    while (x >= e.ex) {
+      x -= e.ex;
+      if (++y == e.ey) {
+        y = 0;
+        ++z;
+      }
+    }
+  }
+}
+
 // Compress: origin fix-up (*:global), count scan and outlier gather.  Thread t
 // owns blocks t*IPT .. t*IPT+IPT-1 of its chunk.  Order of work:
 //  1. counts from the records (shared memory) -> chunk scan -> the aggregate
@@ -308,6 +385,9 @@ __device__ __forceinline__ void regen_blocks(const ScanArgs& a, const int64_t (&
 #ifndef VLZ_SCAN_HB
 #define VLZ_SCAN_HB 1  // heavy blocks regenerated together by a warp (2: 193 us, 4: 358 us on the
                        // outlier-stress field against 155 us -- the register arrays spill)
+#endif
+#ifndef VLZ_SCAN_LANE_REGEN
+#define VLZ_SCAN_LANE_REGEN 8  // lanes of a warp with dense blocks from which each regenerates its own
 #endif
 #ifndef VLZ_SCAN_MINB
 #define VLZ_SCAN_MINB 3
@@ -517,6 +597,14 @@ __global__ void __launch_bounds__(SCAN_THREADS, VLZ_SCAN_MINB) dq_scan_kernel(Sc
   int hl[NB];
   int cnt = 0;
   unsigned hm = __ballot_sync(FULL, heavy != 0);
+  if (__popc(hm) >= VLZ_SCAN_LANE_REGEN) {
+    // most lanes own dense blocks: every lane regenerates its own
+#pragma unroll
+    for (int k = 0; k < SCAN_IPT; ++k)
+      if ((heavy >> k) & 1u)
+        regen_lane(a, base + (int64_t)tid * SCAN_IPT + k, fix ? 1 : 0, outc + dst[k], lim - dst[k]);
+    hm = 0;
+  }
   while (hm) {
     const int src_lane = __ffs(hm) - 1;
     hm &= hm - 1;
