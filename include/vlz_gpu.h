@@ -136,7 +136,10 @@ int vlz_dq_compress_capped(const float* d_in, const vlz_geom* g, const vlz_param
  * postquant + block/edge padding; for *:global policies it also writes this
  * shard's partial statistics to d_stats and leaves block origins pending.
  * The caller all-reduces d_stats (NCCL) and then calls finish, which resolves
- * the global scalar, the origin codes and compacts the outliers. */
+ * the global scalar, the origin codes and compacts the outliers.  d_in, the
+ * codes and the workspace must stay untouched between begin and finish:
+ * finish reads the values of outlier-dense blocks (more than 8 outliers) back
+ * from d_in at the positions the codes mark. */
 int vlz_dq_compress_begin(const float* d_in, const vlz_geom* g, const vlz_params* p,
                           uint16_t* d_codes, int64_t* d_counts, int64_t* d_scalars,
                           vlz_result* d_result, vlz_stats* d_stats, void* d_ws,

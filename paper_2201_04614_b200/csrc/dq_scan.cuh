@@ -23,6 +23,12 @@
 
 namespace vlz {
 
+#ifndef VLZ_SCAN_LANE_STEP
+#define VLZ_SCAN_LANE_STEP 32  // codes a lane reads per regeneration step
+#endif
+#ifndef VLZ_SCAN_LANE_BATCH
+#define VLZ_SCAN_LANE_BATCH 8  // input loads a lane keeps in flight
+#endif
 constexpr int SCAN_THREADS = 256;
 constexpr int SCAN_MIN_CH = SCAN_THREADS;  // smallest chunk (blocks per CTA)
 
@@ -302,40 +308,43 @@ __device__ __forceinline__ void regen_lane(const ScanArgs& a, int64_t bi, int p0
   const uint16_t* __restrict__ cp = a.codes + bstart;
   const float* __restrict__ in = a.in;
   const bool al = ((bstart & 7) == 0) && ((reinterpret_cast<uintptr_t>(a.codes) & 15) == 0);  // 16-byte aligned code vectors
-  int r = 0, x = 0, y = 0, z = 0;       // rank; coordinates of position i0
-  for (int i0 = 0; i0 < nelem; i0 += 32) {
-    unsigned zm = 0;  // bit j: code i0 + j is an outlier
-    if (al && i0 + 32 <= nelem) {
+  constexpr int STEP = VLZ_SCAN_LANE_STEP;  // codes per step (32 or 64)
+  int r = 0, x = 0, y = 0, z = 0;           // rank; coordinates of position i0
+  for (int i0 = 0; i0 < nelem; i0 += STEP) {
+    unsigned long long zm = 0;  // bit j: code i0 + j is an outlier
+    if (al && i0 + STEP <= nelem) {
+      uint4 w[STEP / 8];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint4 w = *reinterpret_cast<const uint4*>(cp + i0 + 8 * q);
-        const unsigned ws[4] = {w.x, w.y, w.z, w.w};
+      for (int q = 0; q < STEP / 8; ++q) w[q] = *reinterpret_cast<const uint4*>(cp + i0 + 8 * q);
+#pragma unroll
+      for (int q = 0; q < STEP / 8; ++q) {
+        const unsigned ws[4] = {w[q].x, w[q].y, w[q].z, w[q].w};
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
-          zm |= ((ws[t] & 0xffffu) == 0u) ? (1u << (8 * q + 2 * t)) : 0u;
-          zm |= ((ws[t] >> 16) == 0u) ? (1u << (8 * q + 2 * t + 1)) : 0u;
+          zm |= ((ws[t] & 0xffffu) == 0u) ? (1ull << (8 * q + 2 * t)) : 0ull;
+          zm |= ((ws[t] >> 16) == 0u) ? (1ull << (8 * q + 2 * t + 1)) : 0ull;
         }
       }
     } else {
 #pragma unroll 8
-      for (int j = 0; j < 32; ++j)
-        if (i0 + j < nelem && cp[i0 + j] == 0) zm |= 1u << j;
+      for (int j = 0; j < STEP; ++j)
+        if (i0 + j < nelem && cp[i0 + j] == 0) zm |= 1ull << j;
     }
-    if (i0 == 0 && p0) zm &= ~1u;  // the origin is settled from its record
-    // the step's input loads together (8 at a time), then their stores
-    unsigned m = zm;
+    if (i0 == 0 && p0) zm &= ~1ull;  // the origin is settled from its record
+    // the step's input loads together (VB at a time), then their stores
+    constexpr int VB = VLZ_SCAN_LANE_BATCH;
+    unsigned long long m = zm;
     int cur = 0;  // codes of this step the coordinates have advanced over
     while (m) {
-      float val[8];
+      float val[VB];
       int n = 0;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < VB; ++u) {
         val[u] = 0.f;
         if (m) {
-          const int j = __ffs(m) - 1;
+          const int j = __ffsll((long long)m) - 1;
           m &= m - 1;
-          // advance (x, y, z) by j - cur positions
-          x += j - cur;
+          x += j - cur;  // advance (x, y, z) by j - cur positions
           cur = j;
           while (x >= e.ex) {
             x -= e.ex;
@@ -349,14 +358,14 @@ __device__ __forceinline__ void regen_lane(const ScanArgs& a, int64_t bi, int p0
         }
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
+      for (int u = 0; u < VB; ++u)
         if (u < n) {
           if (r < olim) outp[r] = val[u];
           ++r;
         }
     }
     // to the first position of the next step
-    x += 32 - cur;
+    x += STEP - cur;
     while (x >= e.ex) {
       x -= e.ex;
       if (++y == e.ey) {
