@@ -309,7 +309,9 @@ __device__ __forceinline__ void regen_lane(const ScanArgs& a, int64_t bi, int p0
   const float* __restrict__ in = a.in;
   const bool al = ((bstart & 7) == 0) && ((reinterpret_cast<uintptr_t>(a.codes) & 15) == 0);  // 16-byte aligned code vectors
   constexpr int STEP = VLZ_SCAN_LANE_STEP;  // codes per step (32 or 64)
-  int r = 0, x = 0, y = 0, z = 0;           // rank; coordinates of position i0
+  int r = 0, x = 0, y = 0;                  // rank; in-block coordinates of the current position
+  const float* pin = in + origin;           // ... and its element of the input
+  const int64_t row_skip = a.g.D2 - e.ex, plane_skip = (a.g.D1 - e.ey) * a.g.D2;
   for (int i0 = 0; i0 < nelem; i0 += STEP) {
     unsigned long long zm = 0;  // bit j: code i0 + j is an outlier
     if (al && i0 + STEP <= nelem) {
@@ -344,16 +346,18 @@ __device__ __forceinline__ void regen_lane(const ScanArgs& a, int64_t bi, int p0
         if (m) {
           const int j = __ffsll((long long)m) - 1;
           m &= m - 1;
-          x += j - cur;  // advance (x, y, z) by j - cur positions
+          x += j - cur;  // advance by j - cur positions
+          pin += j - cur;
           cur = j;
           while (x >= e.ex) {
             x -= e.ex;
+            pin += row_skip;
             if (++y == e.ey) {
               y = 0;
-              ++z;
+              pin += plane_skip;
             }
           }
-          val[u] = __ldg(in + origin + ((int64_t)z * a.g.D1 + y) * a.g.D2 + x);
+          val[u] = __ldg(pin);
           n = u + 1;
         }
       }
@@ -366,11 +370,13 @@ __device__ __forceinline__ void regen_lane(const ScanArgs& a, int64_t bi, int p0
     }
     // to the first position of the next step
     x += STEP - cur;
+    pin += STEP - cur;
     while (x >= e.ex) {
       x -= e.ex;
+      pin += row_skip;
       if (++y == e.ey) {
         y = 0;
-        ++z;
+        pin += plane_skip;
       }
     }
   }
