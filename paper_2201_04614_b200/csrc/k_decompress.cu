@@ -1,3 +1,4 @@
+#include <cstdlib>
 // k_decompress.cu -- reconstruction kernel instantiations and dispatch.
 //   fast shapes (3-D b=8/16, 2-D b=8/16), uint16 codes, aligned buffers:
 //       dq_decompress_fast_kernel (int32 with exactness check; its warps redo
@@ -57,6 +58,10 @@ static cudaError_t run_d(bool u32, const DecompressArgs& a, cudaStream_t st) {
       cudaError_t e = occupancy(kern, FAST_WARPS * 32, fsmem, per_sm);
       if (e != cudaSuccess) return e;
       if (per_sm < 1) per_sm = 1;
+      {  // (experiments: fewer resident CTAs per SM than the occupancy allows)
+        static const int cap = [] { const char* e = std::getenv("VLZ_DGRID_PER_SM"); return e ? std::atoi(e) : 0; }();
+        if (cap > 0 && cap < per_sm) per_sm = cap;
+      }
       int64_t grid = (int64_t)per_sm * num_sms();
       const int64_t need = (a.g.ntiles + FAST_WARPS - 1) / FAST_WARPS;
       if (grid > need) grid = need;

@@ -5,6 +5,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "dq_compress_fast.cuh"
 #include "launch.cuh"
@@ -65,6 +66,10 @@ cudaError_t run_compress_shape(const CompressArgs& a, cudaStream_t st) {
       cudaError_t e = occupancy(kern, FAST_WARPS * 32, fsmem, per_sm);
       if (e != cudaSuccess) return e;
       if (per_sm < 1) per_sm = 1;
+      {  // (experiments: fewer resident CTAs per SM than the occupancy allows)
+        static const int cap = [] { const char* e = std::getenv("VLZ_CGRID_PER_SM"); return e ? std::atoi(e) : 0; }();
+        if (cap > 0 && cap < per_sm) per_sm = cap;
+      }
       int64_t grid = (int64_t)per_sm * num_sms();
       const int64_t need = (a.g.ntiles + FAST_WARPS - 1) / FAST_WARPS;
       if (grid > need) grid = need;
