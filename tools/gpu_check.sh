@@ -11,7 +11,7 @@ timeout 900 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
 timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench rc=$?" >> $O/bench.err
 timeout 600 python tools/bench_configs.py > $O/configs.jsonl 2> $O/configs.err
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"$KRE" -c 400 --csv --log-file $O/launches.csv \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"$KRE" -c 6000 --csv --log-file $O/launches.csv \
   python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > $O/ncu_bench.log 2>&1
 for f in pytest_gpu.log smoke.log bench.err; do tail -n 3 $O/$f; done
 cat $O/bench.json
