@@ -48,6 +48,7 @@ PROTOTYPES = {
     "vlz_block_count": (_i64, [_P(Geom)]),
     "vlz_scalar_count": (_i64, [_P(Geom), ctypes.c_int32, ctypes.c_int32]),
     "vlz_workspace_size": (ctypes.c_size_t, [_P(Geom)]),
+    "vlz_workspace_size_dense": (ctypes.c_size_t, [_P(Geom)]),
     "vlz_dq_compress": (ctypes.c_int, [_vp, _P(Geom), _P(Params), _vp, _vp, _vp, _vp, _vp, _vp,
                                        ctypes.c_size_t, _vp]),
     "vlz_dq_compress_capped": (ctypes.c_int, [_vp, _P(Geom), _P(Params), _vp, _vp, _i64, _vp, _vp,

@@ -280,12 +280,13 @@ __global__ void __launch_bounds__(D1_WARPS * 32, 4)
           cadd = 0u;
           const int excl = group_excl_scan<LPB>(__popc(om), lane, tot);
           const int64_t bstart = (e0 + (lane - gl) * VPL);  // block start = its first element
-          float* slot = a.scratch + (bstart / B) * SCRATCH_SLOTS + 1;
+          float* slot = a.scratch + scratch_base(a.scratch_dense, bstart, bstart / B) + 1;
+          const int slim = scratch_limit(a.scratch_dense);
           int k = excl;  // rank among the block's non-origin outliers
 #pragma unroll
           for (int j = 0; j < VPL; ++j)
             if ((om >> j) & 1u) {
-              if (k < SCRATCH_SLOTS - 1) slot[k] = v[j];
+              if (k < slim) slot[k] = v[j];
               ++k;
             }
         } else if (lead) {
@@ -311,7 +312,7 @@ __global__ void __launch_bounds__(D1_WARPS * 32, 4)
           int64_t total = tot;
           if (MODE != MODE_GLOBAL) {
             if (o_out) {
-              a.scratch[bi * SCRATCH_SLOTS] = v[0];
+              a.scratch[scratch_base(a.scratch_dense, el, bi)] = v[0];
               total += 1;
             }
             if (MODE == MODE_BLOCK || MODE == MODE_EDGE) a.scalars[bi] = s0;

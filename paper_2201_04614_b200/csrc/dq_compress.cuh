@@ -40,7 +40,8 @@ struct CompressArgs {
   QP q;
   const float* in;
   uint16_t* codes;
-  float* scratch;  // SCRATCH_SLOTS floats per block: outlier slots (vlz_common.cuh)
+  float* scratch;  // outlier slots (vlz_common.cuh)
+  int scratch_dense;  // 1: one slot per element (dense layout)
   int64_t* counts;
   int64_t* scalars;
   float* origin_vals;  // *:global: verbatim origin value per block (workspace, coalesced)
@@ -276,11 +277,12 @@ __device__ __forceinline__ bool compress_tile(const CompressArgs& a, int64_t til
         const int cnt = __popc(om);
         const int excl = group_excl_scan<LPB>(cnt, lane, tot);
         int k = run + excl;
-        float* slot = a.scratch + bi * SCRATCH_SLOTS + 1;
+        float* slot = a.scratch + scratch_base(a.scratch_dense, bstart, bi) + 1;
+        const int slim = scratch_limit(a.scratch_dense);
 #pragma unroll
         for (int j = 0; j < VPL; ++j)
           if ((om >> j) & 1u) {
-            if (k < SCRATCH_SLOTS - 1) slot[k] = v[j];
+            if (k < slim) slot[k] = v[j];
             ++k;
           }
         run += tot;
@@ -363,7 +365,7 @@ __device__ __forceinline__ bool compress_tile(const CompressArgs& a, int64_t til
       const bool out = bad_origin || d > (int64_t)(R - 1) || d < -(int64_t)(R - 1);
       a.codes[bstart] = out ? (uint16_t)0 : (uint16_t)(d + R);
       if (out) {
-        a.scratch[bi * SCRATCH_SLOTS] = v_origin;
+        a.scratch[scratch_base(a.scratch_dense, bstart, bi)] = v_origin;
         total += 1;
       }
     }

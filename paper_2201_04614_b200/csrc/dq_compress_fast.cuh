@@ -380,11 +380,12 @@ __device__ __forceinline__ void fast_tile(const FastArgs& fa, uint32_t tile, con
             int tot;
             const int excl = group_excl_scan<LPB>(__popc(om), lane, tot);
             int k = run + excl;
-            float* slot = a.scratch + bi * SCRATCH_SLOTS + 1;
+            float* slot = a.scratch + scratch_base(a.scratch_dense, bstart, bi) + 1;
+            const int slim = scratch_limit(a.scratch_dense);
 #pragma unroll
             for (int j = 0; j < VPL; ++j)
               if ((om >> j) & 1u) {
-                if (k < SCRATCH_SLOTS - 1) slot[k] = vb[r][j];
+                if (k < slim) slot[k] = vb[r][j];
                 ++k;
               }
             run += tot;
@@ -543,11 +544,12 @@ __device__ __forceinline__ void fast_tile(const FastArgs& fa, uint32_t tile, con
         int tot;
         const int excl = group_excl_scan<LPB>(__popc(om), lane, tot);
         int k = run + excl;
-        float* slot = a.scratch + bi * SCRATCH_SLOTS + 1;
+        float* slot = a.scratch + scratch_base(a.scratch_dense, bstart, bi) + 1;
+        const int slim = scratch_limit(a.scratch_dense);
 #pragma unroll
         for (int j = 0; j < VPL; ++j)
           if ((om >> j) & 1u) {
-            if (k < SCRATCH_SLOTS - 1) slot[k] = v[j];
+            if (k < slim) slot[k] = v[j];
             ++k;
           }
         run += tot;
@@ -688,7 +690,7 @@ __device__ __forceinline__ void fast_tile(const FastArgs& fa, uint32_t tile, con
       const bool o = bad_origin || d > (int64_t)(R - 1) || d < -(int64_t)(R - 1);
       a.codes[bstart] = o ? (uint16_t)0 : (uint16_t)(d + R);
       if (o) {
-        a.scratch[bi * SCRATCH_SLOTS] = v_origin;
+        a.scratch[scratch_base(a.scratch_dense, bstart, bi)] = v_origin;
         total += 1;
       }
     }

@@ -57,6 +57,7 @@ struct ScanArgs {
   uint16_t* codes;
   int64_t* counts;
   float* scratch;
+  int scratch_dense;  // 1: one scratch slot per element (vlz_common.cuh)
   float* out;
   int64_t* offsets;
   int64_t* scalars;
@@ -519,10 +520,11 @@ __global__ void __launch_bounds__(SCAN_THREADS, VLZ_SCAN_MINB) dq_scan_kernel(Sc
       rem[k] = c[k] - (int)((omask >> k) & 1u);
       src[k] = 0;
       if (((wmask >> k) & 1u) || rem[k] > 0) {
-        src[k] = bi * SCRATCH_SLOTS + 1;
-        if ((wmask >> k) & 1u) {
-          int64_t bstart, origin;
+        int64_t bstart = 0, origin;
+        if (a.scratch_dense || ((wmask >> k) & 1u))
           block_of(a.g, bi, a.BZ, a.BY, a.BX, bstart, origin);
+        src[k] = scratch_base(a.scratch_dense, bstart, bi) + 1;
+        if ((wmask >> k) & 1u) {
           a.codes[bstart] = ocode[k];
           if (a.patch_list)
             a.patch_list[atomicAdd(a.patch_count, 1u)] =
@@ -541,7 +543,7 @@ __global__ void __launch_bounds__(SCAN_THREADS, VLZ_SCAN_MINB) dq_scan_kernel(Sc
       if (c[k] > 0) {
         int64_t bstart, origin;
         block_of(a.g, bi, a.BZ, a.BY, a.BX, bstart, origin);
-        src[k] = bi * SCRATCH_SLOTS;
+        src[k] = scratch_base(a.scratch_dense, bstart, bi);
         code0[k] = a.codes[bstart];  // 0: the origin is an outlier in slot 0
       }
     }
@@ -603,9 +605,67 @@ __global__ void __launch_bounds__(SCAN_THREADS, VLZ_SCAN_MINB) dq_scan_kernel(Sc
     for (int k = 0; k < SCAN_IPT; ++k)
       if (t < rem[k] && dst[k] + t < lim) outc[dst[k] + t] = v[k];
   }
-  // heavy blocks (>= HEAVY outliers, more than the block's scratch slots hold):
-  // a whole warp regenerates the values from the codes (0 marks an outlier)
-  // and the input, in canonical order
+  // heavy blocks (>= HEAVY outliers).  Dense scratch: whole-warp copies from
+  // the block's slots, four blocks per batch so that their loads overlap.
+  // Compact scratch (the slots hold 7 + the origin): a warp, or each lane for
+  // its own block when most lanes have one, regenerates the values from the
+  // codes (0 marks an outlier) and the input, in canonical order.
+  if (a.scratch_dense) {
+    constexpr int HB = 4;
+    int bn[HB], bd[HB];
+    int64_t bs[HB];
+    int cnt = 0;
+    auto flush = [&]() {
+      int nmax = 0;
+#pragma unroll
+      for (int u = 0; u < HB; ++u) nmax = (u < cnt && bn[u] > nmax) ? bn[u] : nmax;
+      for (int t0 = 0; t0 < nmax; t0 += 128) {
+        float v[HB][4];
+#pragma unroll
+        for (int u = 0; u < HB; ++u) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int t = t0 + lane + 32 * j;
+            if (u < cnt && t < bn[u]) v[u][j] = __ldg(scratch + bs[u] + t);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < HB; ++u) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int t = t0 + lane + 32 * j;
+            if (u < cnt && t < bn[u] && bd[u] + t < lim) outc[bd[u] + t] = v[u][j];
+          }
+        }
+      }
+      cnt = 0;
+    };
+    unsigned hmd = __ballot_sync(FULL, heavy != 0);
+    while (hmd) {
+      const int src_lane = __ffs(hmd) - 1;
+      hmd &= hmd - 1;
+      const unsigned mk = __shfl_sync(FULL, heavy, src_lane);
+#pragma unroll
+      for (int k = 0; k < SCAN_IPT; ++k) {
+        if (!((mk >> k) & 1u)) continue;  // warp-uniform
+        const int first = __shfl_sync(FULL, (int)((omask >> k) & 1u), src_lane);
+        const int n = __shfl_sync(FULL, c[k], src_lane) - first;
+        const int d0 = __shfl_sync(FULL, dst[k], src_lane);
+        const int64_t sb = __shfl_sync(FULL, src[k], src_lane);
+#pragma unroll
+        for (int u = 0; u < HB; ++u) {
+          if (cnt == u) {
+            bn[u] = n;
+            bd[u] = d0;
+            bs[u] = sb;
+          }
+        }
+        if (++cnt == HB) flush();
+      }
+    }
+    if (cnt) flush();
+    return;
+  }
   constexpr int NB = VLZ_SCAN_HB;
   int64_t hb[NB];
   float* ho[NB];

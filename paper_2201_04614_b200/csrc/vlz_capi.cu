@@ -180,7 +180,7 @@ struct WS {
   size_t bytes;
 };
 
-WS carve(const Geo& g, void* base) {
+WS carve(const Geo& g, void* base, bool dense = false) {
   WS w{};
   char* p = static_cast<char*>(base);
   size_t off = 0;
@@ -199,7 +199,7 @@ WS carve(const Geo& g, void* base) {
   w.offsets = reinterpret_cast<int64_t*>(p + off);
   off += align256((size_t)g.nblocks * 8);
   w.scratch = reinterpret_cast<float*>(p + off);
-  off += align256((size_t)g.nblocks * SCRATCH_SLOTS * 4);
+  off += align256(dense ? (size_t)g.N * 4 : (size_t)g.nblocks * SCRATCH_SLOTS * 4);
   w.bytes = off;
   return w;
 }
@@ -369,6 +369,20 @@ int64_t vlz_scalar_count(const vlz_geom* gg, int32_t kind, int32_t gran) {
   return g.nblocks * gg->nd;
 }
 
+// the dense scratch layout is used when the caller's workspace has room for it
+static bool ws_is_dense(const Geo& gc, size_t ws_bytes) {
+  char* null_base = nullptr;
+  return ws_bytes >= carve(gc, null_base, true).bytes;
+}
+
+size_t vlz_workspace_size_dense(const vlz_geom* gg) {
+  Geo gd, gc;
+  if (!make_geo(gg, gd) || !make_geo(gg, gc, true)) return 0;
+  char* null_base = nullptr;
+  const size_t d = carve(gd, null_base).bytes, c = carve(gc, null_base, true).bytes;
+  return d > c ? d : c;
+}
+
 size_t vlz_workspace_size(const vlz_geom* gg) {
   // large enough for both directions (their tile windows may differ)
   Geo gd, gc;
@@ -400,6 +414,7 @@ __attribute__((visibility("hidden"))) int vlz_internal_compress_begin(const floa
   a.in = d_in;
   a.codes = d_codes;
   a.scratch = w.scratch;
+  a.scratch_dense = ws_is_dense(g, ws_bytes) ? 1 : 0;
   a.counts = d_counts;
   a.scalars = d_scalars;
   a.origin_vals = reinterpret_cast<float*>(w.offsets);  // offsets are unused by compress
@@ -459,6 +474,7 @@ static int finish_impl(const float* d_in, const vlz_geom* gg, const vlz_params* 
   s.codes = d_codes;
   s.counts = d_counts;
   s.scratch = w.scratch;
+  s.scratch_dense = ws_is_dense(g, ws_bytes) ? 1 : 0;
   s.out = d_outliers;
   s.scalars = d_scalars;
   s.lb = w.lb;

@@ -98,11 +98,23 @@ __device__ __forceinline__ void ws_wait(const InitArgs& ia) {
   } while (v != ia.nonce);
 }
 
-// Outlier scratch of the compress path: SCRATCH_SLOTS floats per block (slot 0
-// the block origin, 1.. its other outliers in traversal order).  A block with
-// more outliers than fit keeps only its count; the scan kernel regenerates its
-// values from the codes (code 0 marks them) and the input (dq_scan.cuh).
+// Outlier scratch of the compress path, two layouts chosen by the size of the
+// workspace the caller passes:
+//   compact (vlz_workspace_size): SCRATCH_SLOTS floats per block (slot 0 the
+//     block origin, 1.. its other outliers in traversal order).  A block with
+//     more outliers than fit keeps only its count; the scan kernel regenerates
+//     its values from the codes (code 0 marks them) and the input;
+//   dense (vlz_workspace_size_dense): one float per element, the block's slots
+//     at its position in the code stream -- 4 bytes per element more, and the
+//     scan kernel copies instead of regenerating (outlier-dense data).
 constexpr int SCRATCH_SLOTS = 8;
+__host__ __device__ __forceinline__ long long scratch_base(bool dense, long long bstart,
+                                                           long long bi) {
+  return dense ? bstart : bi * SCRATCH_SLOTS;
+}
+__host__ __device__ __forceinline__ int scratch_limit(bool dense) {  // non-origin slots of a block
+  return dense ? 0x7fffffff : SCRATCH_SLOTS - 1;
+}
 
 // Division of 32-bit unsigned values by a launch-invariant divisor d >= 1
 // (Granlund-Montgomery with the add-shift fix-up; exact for every x < 2^32).

@@ -147,6 +147,9 @@ def _alloc_like(n, dtype, device):
     return torch.empty(max(int(n), 1), dtype=dtype, device=device)
 
 
+DENSE_SCRATCH_MAX = 1 << 26  # elements (256 MB of scratch)
+
+
 class Workspace:
     """Grow-only device workspace cache (one per device)."""
 
@@ -201,8 +204,15 @@ def compress_device(x: torch.Tensor, config: CompressionConfig, eb: float = None
     else:
         out.grid, out.eb, out.radius, out.padding, out.source = grid, eb, config.radius, pol, x
         out._host_result = None
-    wsb = lib.vlz_workspace_size(ctypes.byref(g))
+    # arrays up to DENSE_SCRATCH_MAX elements get the dense scratch layout (one
+    # slot per element: outlier-dense blocks are copied, not regenerated); for
+    # larger ones the 4 bytes per element are not worth it (8 slots per block)
+    wsb = (lib.vlz_workspace_size_dense(ctypes.byref(g)) if n <= DENSE_SCRATCH_MAX
+           else lib.vlz_workspace_size(ctypes.byref(g)))
     ws = workspace if workspace is not None else Workspace.get(wsb, dev)
+    # (the library picks the scratch layout from the size it is told: a cached
+    # workspace grown by an earlier, larger call must not switch it)
+    ws_bytes = ws.numel() if workspace is not None else wsb
     if outlier_capacity is not None and int(outlier_capacity) < 0:
         raise ConfigError("outlier_capacity must be >= 0")
     cap = min(n, int(out.outliers.numel())) if (outlier_capacity is not None or
@@ -211,7 +221,7 @@ def compress_device(x: torch.Tensor, config: CompressionConfig, eb: float = None
         rc = lib.vlz_dq_compress(
             _ptr(x), ctypes.byref(g), ctypes.byref(p), _ptr(out.codes), _ptr(out.outliers),
             _ptr(out.counts), _ptr(out.scalars) if ns else None, _ptr(out.result), _ptr(ws),
-            ws.numel(), _stream(stream),
+            ws_bytes, _stream(stream),
         )
     else:
         if outlier_capacity is not None:
@@ -219,7 +229,7 @@ def compress_device(x: torch.Tensor, config: CompressionConfig, eb: float = None
         rc = lib.vlz_dq_compress_capped(
             _ptr(x), ctypes.byref(g), ctypes.byref(p), _ptr(out.codes), _ptr(out.outliers), cap,
             _ptr(out.counts), _ptr(out.scalars) if ns else None, _ptr(out.result), _ptr(ws),
-            ws.numel(), _stream(stream),
+            ws_bytes, _stream(stream),
         )
     if rc != 0:
         raise RuntimeError(f"vlz_dq_compress failed ({rc})")

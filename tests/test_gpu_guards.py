@@ -86,17 +86,18 @@ LARGE = [
 ]
 
 
+@pytest.mark.parametrize("dense_ws", [False, True])
 @pytest.mark.parametrize("kind,shape,b,pol,eb,radius", LARGE)
-def test_no_out_of_bounds_writes_large_paths(kind, shape, b, pol, eb, radius):
+def test_no_out_of_bounds_writes_large_paths(kind, shape, b, pol, eb, radius, dense_ws):
     prev = M.valid_block_edges()
     M.allow_block_256(True)
     try:
-        _run_guarded(_field(kind, shape, b), b, pol, eb, radius)
+        _run_guarded(_field(kind, shape, b), b, pol, eb, radius, dense_ws)
     finally:
         M.allow_block_256(256 in prev)
 
 
-def _run_guarded(data, b, pol, eb, radius):
+def _run_guarded(data, b, pol, eb, radius, dense_ws=False):
     lib = _lib.load()
     shape = data.shape
     n = data.size
@@ -110,7 +111,9 @@ def _run_guarded(data, b, pol, eb, radius):
     codes, outl = Guarded(2 * n), Guarded(4 * n)
     counts, scal = Guarded(8 * grid.block_count), Guarded(8 * max(ns, 1))
     res = Guarded(64)
-    wsb = int(lib.vlz_workspace_size(ctypes.byref(g)))
+    # the workspace guards cover both scratch layouts: 8 slots per block
+    # (compact) and one slot per element (dense, chosen by the size passed)
+    wsb = int((lib.vlz_workspace_size_dense if dense_ws else lib.vlz_workspace_size)(ctypes.byref(g)))
     ws = Guarded(wsb, fill=0)
     rc = lib.vlz_dq_compress(x.ptr(), ctypes.byref(g), ctypes.byref(p), codes.ptr(), outl.ptr(),
                              counts.ptr(), scal.ptr() if ns else None, res.ptr(), ws.ptr(), wsb,

@@ -238,7 +238,7 @@ def test_fullsize_c4_matches_oracle(oracle):
         _check_full(oracle, d, eb, b, "mean:global", r)
 
 
-def test_outlier_stress_matches_oracle(oracle):
+def test_outlier_stress_matches_oracle(oracle, scratch_layout):
     # C4 field at eb = 1e-5 * range: ~18% outliers at R=512
     d = workloads.gen_c4(128)
     eb = workloads.value_range_eb(d, 1e-5)
@@ -462,11 +462,21 @@ def test_fused_kernels_error_precedence(shape, b):
     assert err.value.index == ovf_at
 
 
+@pytest.fixture(params=["compact", "dense"])
+def scratch_layout(request, monkeypatch):
+    # compress_device gives arrays up to gpu.DENSE_SCRATCH_MAX elements the
+    # dense outlier scratch (one slot per element; dense blocks are copied) and
+    # larger ones the compact one (8 slots per block; dense blocks regenerated
+    # from codes + input): force either for the arrays of a test
+    monkeypatch.setattr(gpu, "DENSE_SCRATCH_MAX", 0 if request.param == "compact" else 1 << 40)
+    return request.param
+
+
 @pytest.mark.parametrize("shape,b", [((5000,), 8), ((70001,), 64), ((1 << 20,), 256),
                                      ((4_500_000,), 256), ((45, 300), 8), ((37, 196), 16),
                                      ((100, 516), 32), ((130, 260), 64), ((21, 44, 260), 8),
                                      ((19, 44, 196), 16), ((40, 70, 136), 32), ((70, 130, 136), 64)])
-def test_dense_blocks_regenerated_from_codes(oracle, shape, b):
+def test_dense_blocks_regenerated_from_codes(oracle, shape, b, scratch_layout):
     # the outlier scratch holds 8 slots per block; blocks with more outliers
     # keep only their count and the scan kernel regenerates the values from the
     # codes and the input (regen_block).  Noise far above radius * 2eb makes
@@ -492,7 +502,7 @@ def test_dense_blocks_regenerated_from_codes(oracle, shape, b):
 
 @pytest.mark.parametrize("shape,b,pol", [((40, 72, 256), 8, "mean:global"), ((300, 516), 16, "zero"),
                                          ((1 << 20,), 64, "max:block")])
-def test_capped_outlier_array(oracle, shape, b, pol):
+def test_capped_outlier_array(oracle, shape, b, pol, scratch_layout):
     # vlz_dq_compress_capped: an outlier array sized to the stream (not to the
     # worst case).  Enough capacity: the same stream as the oracle's.  Too
     # little: codes / counts / scalars complete, the first `capacity` outliers
