@@ -117,8 +117,9 @@ def load():
             )
         lib = ctypes.CDLL(LIB_PATH)
         for name, (res, args) in PROTOTYPES.items():
-            if os.environ.get("VLZ_LIB") and name.startswith("vlz_test_") and \
-                    not hasattr(lib, name):
+            if os.environ.get("VLZ_LIB") and not hasattr(lib, name) and \
+                    name.startswith(("vlz_test_", "vlz_bench_", "vlz_workspace_size_dense",
+                                     "vlz_dq_compress_capped")):
                 continue  # an older build under A/B comparison (tools/ab_lib.sh)
             fn = getattr(lib, name)
             fn.restype = res
