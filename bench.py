@@ -669,6 +669,8 @@ def stream_mix(x, codes, y):
     from paper_2201_04614_b200 import _lib
 
     lib = _lib.load()
+    if not hasattr(lib, "vlz_bench_stream"):  # an older build under A/B (VLZ_LIB)
+        return None
     n = (x.numel() // 8) * 8
     st = torch.cuda.current_stream().cuda_stream
     out = {}
