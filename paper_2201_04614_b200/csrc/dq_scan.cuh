@@ -412,7 +412,11 @@ template <int SCAN_IPT>
 __global__ void __launch_bounds__(SCAN_THREADS, VLZ_SCAN_MINB) dq_scan_kernel(ScanArgs a) {
   pdl_enter();
   constexpr int SCAN_CH = SCAN_THREADS * SCAN_IPT;
-  constexpr int HEAVY = VLZ_SCAN_HEAVY;  // blocks with >= HEAVY scratch outliers: whole-warp copy
+  // blocks with >= HEAVY outliers besides a register-held origin: copied by
+  // whole warps (dense scratch) or regenerated (compact scratch, whose slots
+  // hold at most SCRATCH_SLOTS - 1 of them)
+  constexpr int HEAVY = VLZ_SCAN_HEAVY;
+  static_assert(HEAVY >= 2 && HEAVY <= SCRATCH_SLOTS, "light blocks must fit the compact scratch slots");
   // padded so that both the coalesced ([k][tid]) and the per-thread
   // ([tid][k]) access patterns are (nearly) bank-conflict free
   __shared__ long long s_rec[SCAN_CH + SCAN_THREADS];  // count records in, final counts out
