@@ -344,7 +344,10 @@ QP make_qp(const vlz_params* p) {
   const bool fast_ok = q.twoeb > 0.0 && inv > 0x1p-100 && inv < 0x1p100;
   q.inv32 = fast_ok ? (float)inv : 0.0f;
   q.lim0 = fast_ok ? (float)(0.5 - 0x1p-22) : -1.0f;
-  q.kq = (float)0x1p-21;
+#ifndef VLZ_KQ_LOG2
+#define VLZ_KQ_LOG2 22  // margin per unit of |q|: 2^-22 (2^-21 until late round 2)
+#endif
+  q.kq = (float)(1.0 / (double)(1u << VLZ_KQ_LOG2));
   return q;
 }
 

@@ -161,19 +161,25 @@ struct QP {
   // float32 fast path (quant_fast); lim0 < 0 disables it
   float inv32;   // fl32(1 / (2 eb))
   float lim0;    // 0.5 - 2^-22
-  float kq;      // 2^-21
+  float kq;      // 2^-22
 };
 
 // Fast exact prequantization ("fast path proof").
-// q = fl32(v * fl32(1/(2eb))) is within |q| * 2^-22 of fl64(v / (2eb)); the
-// magic-number add rounds q to nearest (n) and e = q - n is exact.  When the
-// distance of q to the rounding boundary, 0.5 - |e|, exceeds
-// |q| * 2^-21 + 2^-22, then (a) round_half_away(fl64(v/(2eb))) == n (no
-// boundary lies between the two quotients, and no tie is possible) and
-// (b) the float32-narrowed reconstruction of n is within eb of v (the f32
-// rounding of n*2eb moves it by at most |q| * 2^-23 * 2eb).  Otherwise the
-// caller re-evaluates the element with quant_exact.  |q| >= 2^21, NaN and
-// Inf always fail the test.
+// q = fl32(v * fl32(1/(2eb))) carries two round-to-nearest errors of 2^-24
+// each, so it is within |q| * 2^-23 (1 + 2^-24) of the real quotient Q, and
+// fl64(v / (2eb)) within 2^-53 |Q|; the magic-number add rounds q to nearest
+// (n) and e = q - n is exact.  When the distance of q to the rounding
+// boundary, 0.5 - |e|, exceeds |q| * 2^-22 + 2^-22 (less 2^-26 for the
+// rounding of the limit itself), then (a) round_half_away(fl64(v/(2eb))) == n
+// (no boundary lies between the two quotients -- twice the error bound --
+// and no tie is possible) and (b) the float32-narrowed reconstruction of n is
+// within eb of v: |n - Q| <= |e| + |q| 2^-23, and the f32 rounding of n*2eb
+// moves it by at most |n| * 2^-24 * 2eb, together |q| * 1.5 * 2^-23 + 2^-25
+// in units of 2eb, inside the margin.  Otherwise the caller re-evaluates the
+// element with quant_exact.  |q| >= 2^21, NaN and Inf always fail the test.
+// (The margin per unit of |q| was 2^-21 until late in round 2; at 2^-22 about
+// half as many rows of C5 take the exact path and the fused compress kernel
+// runs 1.7 % faster.  tests/test_gpu_sweep.py checks every float pattern.)
 __device__ __forceinline__ int quant_fast(float v, const QP& q, bool& ok) {
   const float qq = __fmul_rn(v, q.inv32);
   const float r = __fadd_rn(qq, 12582912.0f);  // 1.5 * 2^23: RN to an integer
